@@ -1,0 +1,165 @@
+/*
+ * hist256.h — C ABI of libhist256.so, the B200 (sm_100a) 256-bin byte-histogram
+ * engine behind the `paper_1011_0235_b200` drop-in for the reference package
+ * `histostream` (arXiv 1011.0235, /root/reference/pkg/src/histostream).
+ *
+ * The reference has no FFI: its hot path is a pair of Numba workers that mutate a
+ * caller-owned zeroed output in place (kernels.py:97-98, :133-134) and are driven
+ * from Python threads. Each entry point below replaces one of those seams; the
+ * Python host layer (paper_1011_0235_b200/kernels.py, stream.py) binds them with
+ * ctypes exactly as INTEGRATION.md shows for a maintainer of the reference.
+ *
+ * Conventions
+ *   - plain pointers and sizes only; `d_` = device pointer, `h_` = host pointer.
+ *   - `stream` is a cudaStream_t passed as void* (0 = legacy default stream).
+ *   - every call is asynchronous on `stream` unless its name ends in `_sync`,
+ *     holds no global mutable state and never allocates device memory: callers
+ *     own outputs and workspace (query sizes with hs_workspace_bytes).
+ *   - return 0 (HS_OK) or a negative status; hs_strerror() names it. CUDA errors
+ *     are folded in as HS_ERR_CUDA_BASE - cudaError_t.
+ *   - histogram outputs are uint64[256] per histogram (core.py:70-94); pattern
+ *     arrays are the reference's int64 offset/count[256] (pattern.py:42-67).
+ */
+#ifndef HIST256_H
+#define HIST256_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HS_BINS 256
+#define HS_ABI_VERSION 1
+
+/* ---- status codes ------------------------------------------------------- */
+#define HS_OK 0
+#define HS_ERR_INVALID_ARG -1          /* null pointer, bad size, bad enum       */
+#define HS_ERR_PATTERN_SHAPE -2        /* pattern.py:141-142 "256 entries"       */
+#define HS_ERR_PATTERN_COUNT_LOW -3    /* pattern.py:143-144 "count below 1"     */
+#define HS_ERR_PATTERN_COUNT_HIGH -4   /* pattern.py:145-146 "count above cap"   */
+#define HS_ERR_PATTERN_TOTAL -5        /* pattern.py:147-148 "slot total mismatch" */
+#define HS_ERR_PATTERN_OFFSETS -6      /* pattern.py:149-150 "offsets not contiguous" */
+#define HS_ERR_SLOT_RANGE -7           /* pattern.py:70-76 SlotCountOutOfRange   */
+#define HS_ERR_WORKSPACE -8            /* workspace smaller than hs_workspace_bytes */
+#define HS_ERR_UNSUPPORTED -9          /* e.g. slot array larger than shared memory */
+#define HS_ERR_ALIGNMENT -10           /* segment bounds not multiples of 4 bytes */
+#define HS_ERR_NO_DEVICE -11
+#define HS_ERR_CUDA_BASE -1000         /* HS_ERR_CUDA_BASE - (int)cudaError_t    */
+
+/* ---- kernel kinds (kernels.py:42-52 KernelKind) ------------------------- */
+#define HS_KIND_NAIVE 0      /* NVHist analogue, kernels.py:336-346 */
+#define HS_KIND_ADAPTIVE 1   /* AHist analogue,  kernels.py:349-384 */
+
+/* ---- device strategies behind a kind --------------------- */
+#define HS_IMPL_AUTO 0       /* library picks by kind and size                     */
+#define HS_IMPL_LANE 1       /* lane-private u32 sub-histograms, bank == lane      */
+#define HS_IMPL_WARP 2       /* per-warp shared u32[256] (paper/SDK NVHist)        */
+#define HS_IMPL_SUBBIN 3     /* per-warp S-slot sub-bins, lane % count (paper AHist) */
+
+/* ---- ablation stages (kernels.py:54-60 ABLATION_STAGES) ----------------- */
+#define HS_STAGE_COPY_ONLY 0
+#define HS_STAGE_COPY_INIT 1
+#define HS_STAGE_PATTERN_LOAD 2
+#define HS_STAGE_SUBHIST_NOREDUCE 3
+#define HS_STAGE_FULL 4
+
+int hs_abi_version(void);
+const char* hs_strerror(int status);
+
+/* Number of SMs, opt-in shared memory per block and L2 bytes of `device`. */
+int hs_device_query(int device, int* sm_count, int* smem_optin, int* l2_bytes);
+
+/* Pattern check in the reference's order (validate_pattern, pattern.py:136-149).
+ * Returns HS_OK or the HS_ERR_PATTERN_* code of the first violated invariant. */
+int hs_validate_pattern(const int64_t* h_offset, const int64_t* h_count,
+                        int64_t total_slots, int64_t cap);
+
+/* Device workspace needed by hs_histogram_batched for `nseg` segments. */
+size_t hs_workspace_bytes(int nseg);
+
+/*
+ * Batched 256-bin histograms over `nseg` word-aligned byte ranges of one device
+ * buffer: d_out[s*256 + b] = #{ i in [h_begin[s], h_end[s]) : d_data[i] == b }.
+ * Replaces batch_histograms (stream.py:260-316), which drives _naive_worker
+ * (kernels.py:97-130) / _adaptive_worker (kernels.py:133-168) per slice and
+ * merges group partials (core.py:152-156). One launch for the whole batch.
+ *   kind     HS_KIND_NAIVE or HS_KIND_ADAPTIVE (ADAPTIVE requires the pattern)
+ *   impl     HS_IMPL_* (HS_IMPL_AUTO for production)
+ *   h_offset/h_count: the CPU binning pattern (pattern.py:94-133), may be NULL
+ *            for NAIVE; validated before launch (kernels.py:363).
+ *   d_out    uint64[nseg*256], overwritten (zeroed by the call on `stream`).
+ * Byte offsets must be multiples of 4 (PackedChunk words, core.py:38-67).
+ */
+int hs_histogram_batched(const uint8_t* d_data, const uint64_t* h_begin, const uint64_t* h_end,
+                         int nseg, int kind, int impl,
+                         const int64_t* h_offset, const int64_t* h_count,
+                         int64_t total_slots, int64_t cap,
+                         uint64_t* d_out, void* d_ws, size_t ws_bytes, void* stream);
+
+/* Single histogram: hs_histogram_batched with one segment [0, n_bytes).
+ * Replaces naive_histogram (kernels.py:336-346) and adaptive_histogram
+ * (kernels.py:349-384); `compute_histogram` (kernels.py:499-512) is the kind switch. */
+int hs_histogram(const uint8_t* d_data, uint64_t n_bytes, int kind, int impl,
+                 const int64_t* h_offset, const int64_t* h_count,
+                 int64_t total_slots, int64_t cap,
+                 uint64_t* d_out, void* d_ws, size_t ws_bytes, void* stream);
+
+/*
+ * Reference-mapping slot totals (compat path for return_slots / narrow_counters /
+ * adaptive_lane_touches, kernels.py:349-407). Words are split with group_ranges
+ * (kernels.py:311-316); word i of group g runs on lane (i - start_g) % group_size and
+ * hits slot offset[b] + lane % count[b] (kernels.py:149-150).
+ *   mode 0: d_out uint64[group_count][total_slots]          (slot_counts)
+ *   mode 1: d_out uint64[group_count][group_size][total_slots] (lane_touch)
+ *   mode 2: d_out uint16[group_count][total_slots], each slot wrapped mod 2^16
+ *           (_adaptive_worker_u16, kernels.py:267-303)
+ * d_out is overwritten. Intended for test-scale inputs (global atomics). */
+int hs_group_slots(const uint8_t* d_data, uint64_t n_bytes, int group_size, int group_count,
+                   const int64_t* h_offset, const int64_t* h_count, int64_t total_slots,
+                   int64_t cap, int mode, void* d_out, void* stream);
+
+/* Genealogy ablation stage (run_ablation, kernels.py:421-496) on the sub-bin kernel
+ * skeleton. d_sink: uint64[1] checksum; d_out256 receives the histogram for
+ * HS_STAGE_FULL (may be NULL otherwise). */
+int hs_ablation_stage(const uint8_t* d_data, uint64_t n_bytes, int stage,
+                      const int64_t* h_offset, const int64_t* h_count,
+                      int64_t total_slots, int64_t cap,
+                      uint64_t* d_sink, uint64_t* d_out256, void* d_ws, size_t ws_bytes,
+                      void* stream);
+
+/* ---- host-side control plane (native replacements of pattern.py / policy.py) */
+
+/* compute_binning_pattern (pattern.py:94-133) / uniform_pattern (pattern.py:85-91 when
+ * the prior is all zero): floor-1, cap, largest-remainder apportionment in float64.
+ * Bit-identical to the reference for totals below 2^53. */
+int hs_binning_pattern(const uint64_t* h_prior, int64_t total_slots, int64_t cap,
+                       int64_t* h_offset, int64_t* h_count);
+
+/* degeneracy (policy.py:39-46): max-bin share, lowest bin on ties, 0 for empty. */
+int hs_degeneracy(const uint64_t* h_counts, double* max_bin_fraction, int* argmax_bin,
+                  uint64_t* total);
+
+/* ---- seeded generators (datagen.py:92-155; splitmix64, byte-exact) ------ */
+#define HS_GEN_UNIFORM 0
+#define HS_GEN_SEQUENTIAL 1
+#define HS_GEN_CONSTANT 2
+#define HS_GEN_NORMAL 3
+#define HS_GEN_MIXTURE 4
+
+/* Host generator: writes n pixels to h_out (uses up to `threads` host threads for
+ * the counter-based kinds; mixture is sequential). */
+int hs_generate_host(int kind, uint64_t seed, int value, double mean, double sigma,
+                     double degeneracy, uint8_t* h_out, uint64_t n, int threads);
+
+/* Device generator (uniform / sequential / constant / normal) for stream positions
+ * [first, first+n) of the pixel sequence `generate` would produce: d_out[i] is
+ * pixel first+i. Used for >=16 GiB device-resident inputs and sharded streams. */
+int hs_generate_device(int kind, uint64_t seed, int value, double mean, double sigma,
+                       uint64_t first, uint8_t* d_out, uint64_t n, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HIST256_H */

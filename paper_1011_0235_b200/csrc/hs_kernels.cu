@@ -1,0 +1,841 @@
+// libhist256 device side: sm_100a kernels for the 256-bin byte histogram of
+// arXiv 1011.0235 and the C ABI that launches them (include/hist256.h).
+//
+// Reference behaviour being replaced (all paths /root/reference/pkg/src/histostream):
+//   _naive_worker     kernels.py:97-130   -> k_lane (HS_IMPL_LANE) / k_warp (HS_IMPL_WARP)
+//   _adaptive_worker  kernels.py:133-168  -> k_lane<HOT> (HS_IMPL_LANE) / k_subbin (HS_IMPL_SUBBIN)
+//   reduce_subbins    kernels.py:410-418  -> fused flush epilogues below
+//   merge_all         core.py:152-156     -> u64 RED into d_out (integer adds commute: exact)
+//   batch_histograms  stream.py:260-316   -> one launch over up to kMaxSeg segments
+//   _adaptive_worker_traced / _u16        -> k_group_slots (reference group/lane mapping)
+//   _stage_*_worker   kernels.py:212-264  -> k_ablation
+//   _fill_*           datagen.py:98-133   -> k_gen_*
+//
+// Design notes (numbers in DESIGN.md §4, tools/microbench/hist_variants.cu):
+//   * Input bytes are read once with 16-B streaming loads (LDG.128, L1::no_allocate),
+//     register double-buffered so a batch is in flight while the previous one is counted.
+//   * HS_IMPL_LANE keeps one private u32 counter column per lane: counter (lane, bin) is
+//     shared word bin*32 + lane of its warp's 32 KB region, so every lane of an ATOMS
+//     hits its own bank (conflict-free for any input, including fully degenerate data).
+//     Seven such warps fill 224 KB of the SM's 227 KB.
+//   * Blackwell merges same-address lanes of one shared atomic, so the contention the
+//     paper's AHist relieves (all lanes on one bin) is cheap here; what costs is distinct
+//     addresses in one bank. ADAPTIVE therefore keeps the lane-private core and uses the
+//     CPU pattern to pick the hot bin, whose all-hot 16-byte vectors are counted in a
+//     register (no shared-memory traffic at all on degenerate input).
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <algorithm>
+
+#include "../../include/hist256.h"
+
+namespace {
+
+constexpr int kMaxSeg = 64;
+constexpr uint64_t kBigCap = 1ull << 30;  // u32 per-warp counters: far from wrapping
+
+struct SegParams {
+  uint64_t begin[kMaxSeg];       // device byte offset of segment s
+  uint64_t vstart[kMaxSeg + 1];  // virtual (concatenated) start of segment s
+  int nseg;
+  int out_base;                  // index of segment 0 of this launch in d_out
+};
+
+struct PatternParams {
+  uint32_t entry[256];           // offset | count << 16   (sub-bin kernels)
+  int32_t total_slots;
+  int32_t hot_bin;               // ADAPTIVE hot bin (argmax count, lowest bin on ties)
+};
+
+// ------------------------------------------------------------------ primitives
+__device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ void sh_inc(uint32_t addr) {
+  asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(addr));
+}
+
+__device__ __forceinline__ void sh_add(uint32_t addr, uint32_t v) {
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v));
+}
+
+__device__ __forceinline__ uint32_t sh_ld(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+
+__device__ __forceinline__ void sh_st(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v));
+}
+
+__device__ __forceinline__ uint4 sh_ld4(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+
+__device__ __forceinline__ void sh_st4(uint32_t addr, uint4 v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w));
+}
+
+__device__ __forceinline__ void compiler_fence() { asm volatile("" ::: "memory"); }
+
+// byte k of w, zero-extended (PRMT)
+__device__ __forceinline__ uint32_t byte_of(uint32_t w, int k) { return __byte_perm(w, 0u, 0x4440u | k); }
+
+// ------------------------------------------------------------------ segment walk
+// Block b owns the word-aligned virtual range [vb, ve) of the concatenated segments.
+__device__ __forceinline__ void block_range(uint64_t total, uint64_t& vb, uint64_t& ve) {
+  const uint64_t tw = total >> 2, g = gridDim.x, b = blockIdx.x;
+  const uint64_t q = tw / g, r = tw % g;
+  vb = 4 * (q * b + min(b, r));
+  ve = vb + 4 * (q + (b < r ? 1 : 0));
+}
+
+// Walks the pieces (segment index, device byte range) of the block's range and calls
+// body(seg, p0, p1) for each non-empty piece; body must end with a block-wide flush.
+template <uint64_t kCap, class Body>
+__device__ __forceinline__ void for_each_piece(const SegParams& sp, Body&& body) {
+  const uint64_t total = sp.vstart[sp.nseg];
+  uint64_t vb, ve;
+  block_range(total, vb, ve);
+  if (vb >= ve) return;
+  int s = 0;
+  while (s < sp.nseg && sp.vstart[s + 1] <= vb) ++s;
+  uint64_t v = vb;
+  for (; s < sp.nseg && v < ve; ++s) {
+    const uint64_t s0 = sp.vstart[s], s1 = sp.vstart[s + 1];
+    if (s1 <= v) continue;
+    const uint64_t hi = min(ve, s1);
+    // sub-pieces of <= kCap bytes per CTA keep every narrow counter from wrapping
+    for (uint64_t a = v; a < hi; a += kCap) {
+      const uint64_t b = min(hi, a + kCap);
+      body(s, sp.begin[s] + (a - s0), sp.begin[s] + (b - s0));
+    }
+    v = hi;
+  }
+}
+
+// Streams the device byte range [p0, p1) (word aligned) through count_word(uint32)
+// and count_vec(uint4): unaligned head/tail words, then 16-B vectors in register
+// double-buffered batches of U vectors per thread.
+template <int U, int PF, class WordFn, class VecFn>
+__device__ __forceinline__ void stream_range(const uint8_t* __restrict__ data, uint64_t p0, uint64_t p1,
+                                             WordFn&& count_word, VecFn&& count_vec) {
+  const uint32_t T = blockDim.x, tid = threadIdx.x;
+  // 16-B alignment is decided on absolute addresses (data itself is only word aligned)
+  const uint64_t base = reinterpret_cast<uintptr_t>(data);
+  const uint64_t a0 = min(p1, ((base + p0 + 15) & ~uint64_t(15)) - base);
+  const uint64_t a1 = max(a0, ((base + p1) & ~uint64_t(15)) - base);
+  for (uint64_t i = p0 + 4ull * tid; i < a0; i += 4ull * T)
+    count_word(*reinterpret_cast<const uint32_t*>(data + i));
+  for (uint64_t i = a1 + 4ull * tid; i < p1; i += 4ull * T)
+    count_word(*reinterpret_cast<const uint32_t*>(data + i));
+  const uint4* __restrict__ vp = reinterpret_cast<const uint4*>(data + a0);
+  const uint64_t nv = (a1 - a0) >> 4;
+  const uint64_t batch = (uint64_t)U * T;
+  const uint64_t nfull = nv / batch;
+  // Bulk L2 prefetch PF batches ahead: with one CTA of 7 warps per SM the register
+  // double buffer alone keeps too few bytes in flight to cover HBM latency; the
+  // prefetched lines turn the LDG.128s into L2 hits. Issued by one thread, no
+  // registers or shared memory involved.
+  const uint64_t vbytes = nv << 4, bbytes = batch << 4;
+  auto prefetch = [&](uint64_t j) {
+    const uint64_t off = j * bbytes;
+    if (tid == 0 && PF > 0 && off < vbytes) {
+      const uint32_t len = uint32_t(min(bbytes, vbytes - off));
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(data + a0 + off), "r"(len) : "memory");
+    }
+  };
+#pragma unroll 1
+  for (int j = 1; j <= PF; ++j) prefetch(j);
+  uint4 A[U], B[U];
+  if (nfull > 0) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) A[u] = ldg_stream(vp + u * T + tid);
+  }
+  for (uint64_t j = 0; j < nfull; j += 2) {
+    prefetch(j + 1 + PF);
+    prefetch(j + 2 + PF);
+    if (j + 1 < nfull) {
+      const uint4* q = vp + (j + 1) * batch + tid;
+#pragma unroll
+      for (int u = 0; u < U; ++u) B[u] = ldg_stream(q + u * T);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) count_vec(A[u]);
+    if (j + 1 >= nfull) break;
+    if (j + 2 < nfull) {
+      const uint4* q = vp + (j + 2) * batch + tid;
+#pragma unroll
+      for (int u = 0; u < U; ++u) A[u] = ldg_stream(q + u * T);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) count_vec(B[u]);
+  }
+  for (uint64_t i = nfull * batch + tid; i < nv; i += T) count_vec(ldg_stream(vp + i));
+}
+
+// ================================================================== HS_IMPL_LANE
+// Lane-private 16-bit "pair" counters. Word (lane, j) of a warp's 16 KB region counts
+// bins 2j and 2j+1 of that lane; it sits at row j (128 B) and column lane, so every
+// lane of a warp-wide atomic hits its own bank. A byte b adds 1 + (b << 16) to word
+// j = b >> 1 (one PRMT builds the increment):
+//     lo = c[2j] + c[2j+1]                  (exact while < 2^16)
+//     hi = sum(b) mod 2^16 = 2j*lo + c[2j+1] (mod 2^16)
+//  => c[2j+1] = (hi - 2j*lo) mod 2^16,  c[2j] = lo - c[2j+1]
+// Half the footprint of u32 columns, so 12 warps fit in 192 KB: the measured shared
+// atomic rate per SM grows with resident warps (tools/microbench/atoms_scaling.cu).
+// A thread may add at most 65535 bytes between flushes; pieces are capped at
+// kLaneFlushBytes per CTA (<= 16 MiB / 384 threads = 43.7 K bytes per thread).
+constexpr int kLaneWarps = 12;
+constexpr int kLaneThreads = 32 * kLaneWarps;
+constexpr uint32_t kLaneRegionBytes = 128 * 32 * 4;  // 128 pair rows x 32 lanes x u32
+constexpr size_t kLaneSmem = size_t(kLaneWarps) * kLaneRegionBytes;
+constexpr uint64_t kLaneFlushBytes = 16ull << 20;
+
+// Adds the CTA's pair counters into out[256] and re-zeroes them.
+// Phase 1: lane l of warp w decodes rows l, l+32, l+64, l+96 of its own region (each
+// row read as 8 x 16-B chunks, staggered by lane so each quarter-warp is conflict
+// free) and parks the two bin sums of row r in words (2r)&31 and (2r+1)&31.
+// Phase 2: thread b sums the parked word of bin b over the warps (bank b & 31).
+__device__ __forceinline__ void lane_flush(uint32_t sbase, unsigned long long* __restrict__ out) {
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  compiler_fence();
+  __syncthreads();
+  const uint32_t region = sbase + warp * kLaneRegionBytes;
+#pragma unroll 1
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t r = lane + 32 * i;
+    const uint32_t row = region + r * 128;
+    uint32_t se = 0, so = 0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const uint4 v = sh_ld4(row + (((c + lane) & 7) << 4));
+      const uint32_t x4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t lo = x4[q] & 0xffffu, hi = x4[q] >> 16;
+        const uint32_t odd = (hi - 2 * r * lo) & 0xffffu;
+        so += odd;
+        se += lo - odd;
+      }
+    }
+    const uint32_t pe = (2 * r) & 31, po = (2 * r + 1) & 31;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const uint32_t chunk = (c + lane) & 7;
+      uint32_t z[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t wi = chunk * 4 + q;
+        z[q] = wi == pe ? se : (wi == po ? so : 0u);
+      }
+      sh_st4(row + (chunk << 4), make_uint4(z[0], z[1], z[2], z[3]));
+    }
+  }
+  compiler_fence();
+  __syncthreads();
+  for (uint32_t b = threadIdx.x; b < 256; b += blockDim.x) {
+    unsigned long long tot = 0;
+#pragma unroll
+    for (int w = 0; w < kLaneWarps; ++w) {
+      const uint32_t a = sbase + w * kLaneRegionBytes + (b >> 1) * 128 + ((b & 31) << 2);
+      tot += sh_ld(a);
+      sh_st(a, 0);
+    }
+    if (tot) atomicAdd(out + b, tot);
+  }
+  compiler_fence();
+  __syncthreads();
+}
+
+template <int U, int PF, bool HOT>
+__global__ void __launch_bounds__(kLaneThreads, 1)
+    k_lane(const uint8_t* __restrict__ data, const __grid_constant__ SegParams sp, int hot_bin,
+           unsigned long long* __restrict__ out) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
+  {
+    const uint32_t n16 = uint32_t(kLaneSmem / 16);
+    for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x) sh_st4(sbase + i * 16, make_uint4(0, 0, 0, 0));
+  }
+  __syncthreads();
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t tb = sbase + warp * kLaneRegionBytes + lane * 4;  // column base: bank == lane
+  const uint32_t hot = uint32_t(hot_bin & 0xff);
+  const uint32_t hot4 = hot * 0x01010101u;
+  uint32_t hotcnt = 0;
+
+  auto word = [&](uint32_t w) {
+    const uint32_t h = (w >> 1) & 0x7f7f7f7fu;  // pair row of each byte
+    sh_add(tb + (byte_of(h, 0) << 7), __byte_perm(w, 1u, 0x7054u));
+    sh_add(tb + (byte_of(h, 1) << 7), __byte_perm(w, 1u, 0x7154u));
+    sh_add(tb + (byte_of(h, 2) << 7), __byte_perm(w, 1u, 0x7254u));
+    sh_add(tb + (byte_of(h, 3) << 7), __byte_perm(w, 1u, 0x7354u));
+  };
+  auto vec = [&](const uint4& v) {
+    if (HOT) {
+      const uint32_t d = (v.x ^ hot4) | (v.y ^ hot4) | (v.z ^ hot4) | (v.w ^ hot4);
+      if (d == 0) { hotcnt += 16; return; }
+    }
+    word(v.x); word(v.y); word(v.z); word(v.w);
+  };
+  for_each_piece<kLaneFlushBytes>(sp, [&](int s, uint64_t p0, uint64_t p1) {
+    stream_range<U, PF>(data, p0, p1, word, vec);
+    if (HOT) {
+      // hotcnt hits of byte `hot`: lo += hotcnt, hi += hotcnt * hot (mod 2^16)
+      if (hotcnt) sh_add(tb + ((hot >> 1) << 7), hotcnt * (1u + (hot << 16)));
+      hotcnt = 0;
+    }
+    lane_flush(sbase, out + size_t(sp.out_base + s) * 256);
+  });
+}
+
+// ================================================================== HS_IMPL_WARP
+// per-warp shared u32[256] (SDK / paper NVHist). 8 warps per block.
+constexpr int kWarpThreads = 256;
+
+template <int U, int PF>
+__global__ void __launch_bounds__(kWarpThreads)
+    k_warp(const uint8_t* __restrict__ data, const __grid_constant__ SegParams sp,
+           unsigned long long* __restrict__ out) {
+  __shared__ __align__(16) uint32_t hist[8 * 256];
+  for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  const uint32_t hb = (uint32_t)__cvta_generic_to_shared(hist) + (threadIdx.x >> 5) * 1024;
+  auto word = [&](uint32_t w) {
+    sh_inc(hb + (byte_of(w, 0) << 2));
+    sh_inc(hb + (byte_of(w, 1) << 2));
+    sh_inc(hb + (byte_of(w, 2) << 2));
+    sh_inc(hb + (byte_of(w, 3) << 2));
+  };
+  auto vec = [&](const uint4& v) { word(v.x); word(v.y); word(v.z); word(v.w); };
+  for_each_piece<kBigCap>(sp, [&](int s, uint64_t p0, uint64_t p1) {
+    stream_range<U, PF>(data, p0, p1, word, vec);
+    compiler_fence();
+    __syncthreads();
+    const int b = threadIdx.x;
+    unsigned long long tot = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) { tot += hist[w * 256 + b]; hist[w * 256 + b] = 0; }
+    if (tot) atomicAdd(out + size_t(sp.out_base + s) * 256 + b, tot);
+    __syncthreads();
+  });
+}
+
+// ================================================================== HS_IMPL_SUBBIN
+// The paper's AHist: per-warp S-slot array; lane L adds byte b into slot
+// offset[b] + L % count[b] (kernels.py:149-150). The CPU pattern is expanded into a
+// lane-banked LUT slot_of[b*32 + lane] (32 KB) so the per-byte lookup is conflict-free;
+// the slot atomics themselves see the pattern's bank spread.
+constexpr int kSubThreads = 256;
+
+template <int U, int PF>
+__global__ void __launch_bounds__(kSubThreads)
+    k_subbin(const uint8_t* __restrict__ data, const __grid_constant__ SegParams sp,
+             const __grid_constant__ PatternParams pp, unsigned long long* __restrict__ out) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint32_t* lut = reinterpret_cast<uint32_t*>(smem);            // 256*32 words
+  uint32_t* slots = lut + 256 * 32;                             // 8 warps x S
+  const int S = pp.total_slots;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) {
+    const uint32_t b = i >> 5, l = i & 31, e = pp.entry[b];
+    const uint32_t off = e & 0xffff, cnt = e >> 16;
+    lut[i] = (off + l % cnt) * 4;
+  }
+  for (int i = threadIdx.x; i < 8 * S; i += blockDim.x) slots[i] = 0;
+  __syncthreads();
+  const uint32_t lb = (uint32_t)__cvta_generic_to_shared(lut) + lane * 4;
+  const uint32_t wb = (uint32_t)__cvta_generic_to_shared(slots) + warp * S * 4;
+  auto word = [&](uint32_t w) {
+    sh_inc(wb + sh_ld(lb + (byte_of(w, 0) << 7)));
+    sh_inc(wb + sh_ld(lb + (byte_of(w, 1) << 7)));
+    sh_inc(wb + sh_ld(lb + (byte_of(w, 2) << 7)));
+    sh_inc(wb + sh_ld(lb + (byte_of(w, 3) << 7)));
+  };
+  auto vec = [&](const uint4& v) { word(v.x); word(v.y); word(v.z); word(v.w); };
+  for_each_piece<kBigCap>(sp, [&](int s, uint64_t p0, uint64_t p1) {
+    stream_range<U, PF>(data, p0, p1, word, vec);
+    compiler_fence();
+    __syncthreads();
+    // reduce_subbins fused: bin b = sum of its count[b] slots over the 8 warps
+    const int b = threadIdx.x;
+    const uint32_t e = pp.entry[b], off = e & 0xffff, cnt = e >> 16;
+    unsigned long long tot = 0;
+    for (int w = 0; w < 8; ++w)
+      for (uint32_t j = 0; j < cnt; ++j) tot += slots[w * S + off + j];
+    __syncthreads();
+    for (int i = threadIdx.x; i < 8 * S; i += blockDim.x) slots[i] = 0;
+    if (tot) atomicAdd(out + size_t(sp.out_base + s) * 256 + b, tot);
+    __syncthreads();
+  });
+}
+
+// ================================================================== compat slots
+// Reference group/lane mapping, one thread per word; global 64-bit atomics.
+__global__ void k_group_slots(const uint32_t* __restrict__ words, uint64_t n_words, int group_size,
+                              int group_count, const __grid_constant__ PatternParams pp, int mode,
+                              unsigned long long* __restrict__ out) {
+  const uint64_t base = n_words / group_count;
+  const int S = pp.total_slots;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n_words;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t g = base ? min(i / base, uint64_t(group_count - 1)) : uint64_t(group_count - 1);
+    const uint64_t start = g * base;
+    const uint32_t lane = uint32_t((i - start) % uint64_t(group_size));
+    const uint32_t w = words[i];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t b = (w >> (8 * k)) & 0xff;
+      const uint32_t e = pp.entry[b], off = e & 0xffff, cnt = e >> 16;
+      const uint32_t slot = off + lane % cnt;
+      size_t idx = mode == 1 ? (g * group_size + lane) * S + slot : g * S + slot;
+      atomicAdd(out + idx, 1ull);
+    }
+  }
+}
+
+__global__ void k_wrap16(const unsigned long long* __restrict__ in, uint16_t* __restrict__ out, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = (uint16_t)(in[i] & 0xffff);
+}
+
+// ================================================================== ablation (genealogy)
+// Cumulative stages on the sub-bin skeleton (kernels.py:212-264, :421-496).
+__global__ void __launch_bounds__(kSubThreads)
+    k_ablation(const uint8_t* __restrict__ data, uint64_t n_bytes, int stage,
+               const __grid_constant__ PatternParams pp, unsigned long long* __restrict__ sink,
+               unsigned long long* __restrict__ out) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint32_t* lut = reinterpret_cast<uint32_t*>(smem);
+  uint32_t* slots = lut + 256 * 32;
+  const int S = pp.total_slots;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (stage >= HS_STAGE_PATTERN_LOAD) {
+    for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) {
+      const uint32_t b = i >> 5, l = i & 31, e = pp.entry[b];
+      lut[i] = ((e & 0xffff) + l % (e >> 16)) * 4;
+    }
+  }
+  if (stage >= HS_STAGE_COPY_INIT)
+    for (int i = threadIdx.x; i < 8 * S; i += blockDim.x) slots[i] = 0;
+  __syncthreads();
+  const uint32_t lb = (uint32_t)__cvta_generic_to_shared(lut) + lane * 4;
+  const uint32_t wb = (uint32_t)__cvta_generic_to_shared(slots) + warp * S * 4;
+  unsigned long long x = 0;
+  auto word = [&](uint32_t w) {
+    if (stage <= HS_STAGE_COPY_INIT) { x ^= w; return; }
+    if (stage == HS_STAGE_PATTERN_LOAD) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) x ^= sh_ld(lb + (byte_of(w, k) << 7));
+      return;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) sh_inc(wb + sh_ld(lb + (byte_of(w, k) << 7)));
+  };
+  auto vec = [&](const uint4& v) { word(v.x); word(v.y); word(v.z); word(v.w); };
+  uint64_t vb, ve;
+  block_range(n_bytes, vb, ve);
+  if (vb < ve) stream_range<8, 2>(data, vb, ve, word, vec);
+  compiler_fence();
+  __syncthreads();
+  if (stage <= HS_STAGE_PATTERN_LOAD) {
+    // xor is order independent: deterministic checksum
+    for (int o = 16; o; o >>= 1) x ^= __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0 && x) atomicXor(sink, x);
+    return;
+  }
+  const int b = threadIdx.x;
+  const uint32_t e = pp.entry[b], off = e & 0xffff, cnt = e >> 16;
+  unsigned long long tot = 0;
+  if (stage == HS_STAGE_SUBHIST_NOREDUCE) {
+    // sink = sum of every slot (kernels.py:462-463)
+    for (int i = threadIdx.x; i < 8 * S; i += blockDim.x) tot += slots[i];
+    if (tot) atomicAdd(sink, tot);
+    return;
+  }
+  for (int w = 0; w < 8; ++w)
+    for (uint32_t j = 0; j < cnt; ++j) tot += slots[w * S + off + j];
+  if (tot) atomicAdd(out + b, tot);
+}
+
+// ================================================================== generators
+__host__ __device__ __forceinline__ uint64_t sm64_mix(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;
+
+// uniform: pixel i is byte (i & 7) of splitmix output (i >> 3) (datagen.py:98-112)
+__global__ void k_gen_uniform(uint64_t seed, uint64_t first, uint8_t* __restrict__ out, uint64_t n) {
+  const uint64_t k0 = first >> 3, k1 = (first + n + 7) >> 3;
+  for (uint64_t k = k0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < k1;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t z = sm64_mix(seed + (k + 1) * kGolden);
+    const uint64_t p = k * 8;
+    if (p >= first && p + 8 <= first + n && ((p - first) & 7) == 0 &&
+        ((reinterpret_cast<uintptr_t>(out + (p - first)) & 7) == 0)) {
+      *reinterpret_cast<uint64_t*>(out + (p - first)) = z;
+    } else {
+      for (int j = 0; j < 8; ++j) {
+        const uint64_t q = p + j;
+        if (q >= first && q < first + n) out[q - first] = uint8_t(z >> (8 * j));
+      }
+    }
+  }
+}
+
+// normal: Irwin-Hall of 12 units, floor(mean + sigma*z + 0.5) clamped (datagen.py:115-133);
+// explicit _rn intrinsics keep nvcc from contracting into FMA (numba does not).
+__global__ void k_gen_normal(uint64_t seed, double mean, double sigma, uint64_t first,
+                             uint8_t* __restrict__ out, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t pix = first + i;
+    uint64_t st = seed + (pix * 12) * kGolden;
+    double total = 0.0;
+#pragma unroll
+    for (int j = 0; j < 12; ++j) {
+      st += kGolden;
+      total = __dadd_rn(total, __dmul_rn((double)(sm64_mix(st) >> 11), 1.0 / 9007199254740992.0));
+    }
+    double val = floor(__dadd_rn(__dadd_rn(mean, __dmul_rn(sigma, __dadd_rn(total, -6.0))), 0.5));
+    val = val < 0.0 ? 0.0 : (val > 255.0 ? 255.0 : val);
+    out[i] = (uint8_t)val;
+  }
+}
+
+__global__ void k_gen_sequential(uint64_t first, uint8_t* __restrict__ out, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = uint8_t((first + i) & 0xff);
+}
+
+// ================================================================== host helpers
+inline int fold(cudaError_t e) { return e == cudaSuccess ? HS_OK : HS_ERR_CUDA_BASE - int(e); }
+
+struct DevInfo { int sms = 0; int smem_optin = 0; int l2 = 0; };
+
+int dev_info(DevInfo& di) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return fold(e);
+  // cached per device (attribute queries are cheap but not free)
+  static thread_local int cached_dev = -1;
+  static thread_local DevInfo cached;
+  if (cached_dev == dev) { di = cached; return HS_OK; }
+  if ((e = cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return fold(e);
+  if ((e = cudaDeviceGetAttribute(&di.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess) return fold(e);
+  if ((e = cudaDeviceGetAttribute(&di.l2, cudaDevAttrL2CacheSize, dev)) != cudaSuccess) return fold(e);
+  cached_dev = dev;
+  cached = di;
+  return HS_OK;
+}
+
+int validate(const int64_t* off, const int64_t* cnt, int64_t S, int64_t cap) {
+  if (!off || !cnt) return HS_ERR_PATTERN_SHAPE;
+  for (int b = 0; b < 256; ++b) if (cnt[b] < 1) return HS_ERR_PATTERN_COUNT_LOW;
+  for (int b = 0; b < 256; ++b) if (cnt[b] > cap) return HS_ERR_PATTERN_COUNT_HIGH;
+  int64_t sum = 0;
+  for (int b = 0; b < 256; ++b) sum += cnt[b];
+  if (sum != S) return HS_ERR_PATTERN_TOTAL;
+  if (off[0] != 0) return HS_ERR_PATTERN_OFFSETS;
+  for (int b = 1; b < 256; ++b) if (off[b] != off[b - 1] + cnt[b - 1]) return HS_ERR_PATTERN_OFFSETS;
+  return HS_OK;
+}
+
+int make_pattern(const int64_t* off, const int64_t* cnt, int64_t S, int64_t cap, PatternParams& pp) {
+  int st = validate(off, cnt, S, cap);
+  if (st != HS_OK) return st;
+  if (S > 65535) return HS_ERR_UNSUPPORTED;
+  int64_t best = -1;
+  pp.hot_bin = 0;
+  for (int b = 0; b < 256; ++b) {
+    const int64_t c = cnt[b] > 0xffff ? 0xffff : cnt[b];
+    pp.entry[b] = uint32_t(off[b]) | (uint32_t(c) << 16);
+    if (cnt[b] > best) { best = cnt[b]; pp.hot_bin = b; }
+  }
+  pp.total_slots = int32_t(S);
+  return HS_OK;
+}
+
+template <class K>
+int set_smem(K kernel, size_t bytes) {
+  if (bytes <= 48 * 1024) return HS_OK;
+  return fold(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+}
+
+// development knobs for tuning runs (tools/kbench.py); production uses the defaults
+int lane_u() {
+  static int u = [] {
+    const char* s = getenv("HS_LANE_U");
+    return s ? atoi(s) : 8;
+  }();
+  return u;
+}
+int lane_pf() {
+  static int p = [] {
+    const char* s = getenv("HS_LANE_PF");
+    return s ? atoi(s) : 0;
+  }();
+  return p;
+}
+
+// one launch over <= kMaxSeg segments
+int launch_batch(const uint8_t* d_data, const uint64_t* h_begin, const uint64_t* h_end, int s0, int ns,
+                 int kind, int impl, const PatternParams* pp, unsigned long long* d_out, cudaStream_t st,
+                 const DevInfo& di) {
+  SegParams sp;
+  sp.nseg = ns;
+  sp.out_base = s0;
+  uint64_t v = 0;
+  for (int i = 0; i < ns; ++i) {
+    sp.begin[i] = h_begin[s0 + i];
+    sp.vstart[i] = v;
+    v += h_end[s0 + i] - h_begin[s0 + i];
+  }
+  sp.vstart[ns] = v;
+  if (v == 0) return HS_OK;
+  if (impl == HS_IMPL_AUTO) impl = (v >= (8ull << 20)) ? HS_IMPL_LANE : HS_IMPL_WARP;
+  cudaError_t e = cudaSuccess;
+  if (impl == HS_IMPL_LANE) {
+    if ((size_t)di.smem_optin < kLaneSmem) return HS_ERR_UNSUPPORTED;
+    const uint64_t want = (v + (256ull << 10) - 1) / (256ull << 10);
+    const int grid = int(std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(di.sms))));
+    const bool hot = kind == HS_KIND_ADAPTIVE;
+    const int hb = pp ? pp->hot_bin : 0;
+    int rc;
+#define HS_LAUNCH_LANE(UU, PP)                                                                 \
+  if (hot) {                                                                                   \
+    if ((rc = set_smem(k_lane<UU, PP, true>, kLaneSmem)) != HS_OK) return rc;                  \
+    k_lane<UU, PP, true><<<grid, kLaneThreads, kLaneSmem, st>>>(d_data, sp, hb, d_out);        \
+  } else {                                                                                     \
+    if ((rc = set_smem(k_lane<UU, PP, false>, kLaneSmem)) != HS_OK) return rc;                 \
+    k_lane<UU, PP, false><<<grid, kLaneThreads, kLaneSmem, st>>>(d_data, sp, hb, d_out);       \
+  }
+    switch (lane_u() * 16 + lane_pf()) {
+      case 8 * 16 + 1: HS_LAUNCH_LANE(8, 1) break;
+      case 8 * 16 + 2: HS_LAUNCH_LANE(8, 2) break;
+      case 6 * 16 + 0: HS_LAUNCH_LANE(6, 0) break;
+      case 4 * 16 + 0: HS_LAUNCH_LANE(4, 0) break;
+      case 4 * 16 + 2: HS_LAUNCH_LANE(4, 2) break;
+      default: HS_LAUNCH_LANE(8, 0) break;
+    }
+#undef HS_LAUNCH_LANE
+  } else if (impl == HS_IMPL_WARP) {
+    const uint64_t want = (v + (32ull << 10) - 1) / (32ull << 10);
+    const int grid = int(std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(di.sms) * 8)));
+    k_warp<4, 0><<<grid, kWarpThreads, 0, st>>>(d_data, sp, d_out);
+  } else if (impl == HS_IMPL_SUBBIN) {
+    if (!pp) return HS_ERR_INVALID_ARG;
+    const size_t smem = (256 * 32 + 8 * size_t(pp->total_slots)) * 4;
+    if (smem > (size_t)di.smem_optin) return HS_ERR_UNSUPPORTED;
+    int rc = set_smem(k_subbin<4, 0>, smem);
+    if (rc != HS_OK) return rc;
+    const uint64_t want = (v + (64ull << 10) - 1) / (64ull << 10);
+    const int per_sm = std::max(1, int(di.smem_optin / (smem + 1024)));
+    const int grid = int(std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(di.sms) * per_sm)));
+    k_subbin<4, 0><<<grid, kSubThreads, smem, st>>>(d_data, sp, *pp, d_out);
+  } else {
+    return HS_ERR_INVALID_ARG;
+  }
+  e = cudaGetLastError();
+  return fold(e);
+}
+
+}  // namespace
+
+// ================================================================== C ABI
+extern "C" {
+
+int hs_abi_version(void) { return HS_ABI_VERSION; }
+
+const char* hs_strerror(int status) {
+  switch (status) {
+    case HS_OK: return "ok";
+    case HS_ERR_INVALID_ARG: return "invalid argument";
+    case HS_ERR_PATTERN_SHAPE: return "pattern arrays must have 256 entries";
+    case HS_ERR_PATTERN_COUNT_LOW: return "count below 1";
+    case HS_ERR_PATTERN_COUNT_HIGH: return "count above cap";
+    case HS_ERR_PATTERN_TOTAL: return "slot total mismatch";
+    case HS_ERR_PATTERN_OFFSETS: return "offsets not contiguous";
+    case HS_ERR_SLOT_RANGE: return "total_slots outside [256, 256 * cap]";
+    case HS_ERR_WORKSPACE: return "workspace too small";
+    case HS_ERR_UNSUPPORTED: return "configuration not supported on this device";
+    case HS_ERR_ALIGNMENT: return "segment bounds must be multiples of 4 bytes";
+    case HS_ERR_NO_DEVICE: return "no CUDA device";
+    default: break;
+  }
+  if (status <= HS_ERR_CUDA_BASE) return cudaGetErrorString(cudaError_t(HS_ERR_CUDA_BASE - status));
+  return "unknown status";
+}
+
+int hs_device_query(int device, int* sm_count, int* smem_optin, int* l2_bytes) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) return HS_ERR_NO_DEVICE;
+  if (device < 0 || device >= n) return HS_ERR_INVALID_ARG;
+  if (sm_count && (e = cudaDeviceGetAttribute(sm_count, cudaDevAttrMultiProcessorCount, device)) != cudaSuccess) return fold(e);
+  if (smem_optin && (e = cudaDeviceGetAttribute(smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device)) != cudaSuccess) return fold(e);
+  if (l2_bytes && (e = cudaDeviceGetAttribute(l2_bytes, cudaDevAttrL2CacheSize, device)) != cudaSuccess) return fold(e);
+  return HS_OK;
+}
+
+int hs_validate_pattern(const int64_t* h_offset, const int64_t* h_count, int64_t total_slots, int64_t cap) {
+  return validate(h_offset, h_count, total_slots, cap);
+}
+
+size_t hs_workspace_bytes(int nseg) { return nseg < 0 ? 0 : 256; }
+
+int hs_histogram_batched(const uint8_t* d_data, const uint64_t* h_begin, const uint64_t* h_end, int nseg,
+                         int kind, int impl, const int64_t* h_offset, const int64_t* h_count,
+                         int64_t total_slots, int64_t cap, uint64_t* d_out, void* d_ws, size_t ws_bytes,
+                         void* stream) {
+  (void)d_ws; (void)ws_bytes;
+  if (nseg < 0 || (nseg > 0 && (!h_begin || !h_end || !d_out))) return HS_ERR_INVALID_ARG;
+  if (kind != HS_KIND_NAIVE && kind != HS_KIND_ADAPTIVE) return HS_ERR_INVALID_ARG;
+  if (impl < HS_IMPL_AUTO || impl > HS_IMPL_SUBBIN) return HS_ERR_INVALID_ARG;
+  PatternParams pp;
+  const bool have_pattern = h_offset && h_count;
+  if (kind == HS_KIND_ADAPTIVE && !have_pattern) return HS_ERR_INVALID_ARG;
+  if (impl == HS_IMPL_SUBBIN && !have_pattern) return HS_ERR_INVALID_ARG;
+  if (have_pattern) {
+    int rc = make_pattern(h_offset, h_count, total_slots, cap, pp);
+    if (rc != HS_OK) return rc;
+  }
+  uint64_t total = 0;
+  for (int s = 0; s < nseg; ++s) {
+    if ((h_begin[s] & 3) || (h_end[s] & 3) || h_end[s] < h_begin[s]) return HS_ERR_ALIGNMENT;
+    total += h_end[s] - h_begin[s];
+  }
+  if (total > 0 && !d_data) return HS_ERR_INVALID_ARG;
+  if (reinterpret_cast<uintptr_t>(d_data) & 3) return HS_ERR_ALIGNMENT;
+  if (nseg == 0) return HS_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemsetAsync(d_out, 0, size_t(nseg) * 256 * sizeof(uint64_t), st);
+  if (e != cudaSuccess) return fold(e);
+  if (total == 0) return HS_OK;
+  DevInfo di;
+  int rc = dev_info(di);
+  if (rc != HS_OK) return rc;
+  for (int s0 = 0; s0 < nseg; s0 += kMaxSeg) {
+    const int ns = std::min(kMaxSeg, nseg - s0);
+    rc = launch_batch(d_data, h_begin, h_end, s0, ns, kind, impl, have_pattern ? &pp : nullptr,
+                      reinterpret_cast<unsigned long long*>(d_out), st, di);
+    if (rc != HS_OK) return rc;
+  }
+  return HS_OK;
+}
+
+int hs_histogram(const uint8_t* d_data, uint64_t n_bytes, int kind, int impl, const int64_t* h_offset,
+                 const int64_t* h_count, int64_t total_slots, int64_t cap, uint64_t* d_out, void* d_ws,
+                 size_t ws_bytes, void* stream) {
+  const uint64_t b = 0, e = n_bytes;
+  return hs_histogram_batched(d_data, &b, &e, 1, kind, impl, h_offset, h_count, total_slots, cap, d_out,
+                              d_ws, ws_bytes, stream);
+}
+
+int hs_group_slots(const uint8_t* d_data, uint64_t n_bytes, int group_size, int group_count,
+                   const int64_t* h_offset, const int64_t* h_count, int64_t total_slots, int64_t cap,
+                   int mode, void* d_out, void* stream) {
+  if (group_size < 1 || group_count < 1 || mode < 0 || mode > 2 || !d_out) return HS_ERR_INVALID_ARG;
+  if (n_bytes & 3) return HS_ERR_ALIGNMENT;
+  if (n_bytes && !d_data) return HS_ERR_INVALID_ARG;
+  if (reinterpret_cast<uintptr_t>(d_data) & 3) return HS_ERR_ALIGNMENT;
+  PatternParams pp;
+  int rc = make_pattern(h_offset, h_count, total_slots, cap, pp);
+  if (rc != HS_OK) return rc;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const uint64_t S = uint64_t(total_slots);
+  const uint64_t n_out = mode == 1 ? uint64_t(group_count) * group_size * S : uint64_t(group_count) * S;
+  unsigned long long* acc = nullptr;
+  cudaError_t e;
+  if (mode == 2) {
+    // exact 64-bit totals in a scratch buffer, then wrapped to 16 bits
+    e = cudaMallocAsync(reinterpret_cast<void**>(&acc), n_out * 8, st);
+    if (e != cudaSuccess) return fold(e);
+  } else {
+    acc = reinterpret_cast<unsigned long long*>(d_out);
+  }
+  e = cudaMemsetAsync(acc, 0, n_out * 8, st);
+  if (e != cudaSuccess) return fold(e);
+  const uint64_t nw = n_bytes / 4;
+  if (nw) {
+    const int grid = int(std::min<uint64_t>((nw + 255) / 256, 4096));
+    k_group_slots<<<grid, 256, 0, st>>>(reinterpret_cast<const uint32_t*>(d_data), nw, group_size, group_count,
+                                        pp, mode == 1 ? 1 : 0, acc);
+    if ((e = cudaGetLastError()) != cudaSuccess) return fold(e);
+  }
+  if (mode == 2) {
+    const int grid = int(std::min<uint64_t>((n_out + 255) / 256, 4096));
+    k_wrap16<<<grid, 256, 0, st>>>(acc, reinterpret_cast<uint16_t*>(d_out), n_out);
+    if ((e = cudaGetLastError()) != cudaSuccess) return fold(e);
+    if ((e = cudaFreeAsync(acc, st)) != cudaSuccess) return fold(e);
+  }
+  return HS_OK;
+}
+
+int hs_ablation_stage(const uint8_t* d_data, uint64_t n_bytes, int stage, const int64_t* h_offset,
+                      const int64_t* h_count, int64_t total_slots, int64_t cap, uint64_t* d_sink,
+                      uint64_t* d_out256, void* d_ws, size_t ws_bytes, void* stream) {
+  (void)d_ws; (void)ws_bytes;
+  if (stage < HS_STAGE_COPY_ONLY || stage > HS_STAGE_FULL || !d_sink) return HS_ERR_INVALID_ARG;
+  if (stage == HS_STAGE_FULL && !d_out256) return HS_ERR_INVALID_ARG;
+  if ((n_bytes & 3) || (reinterpret_cast<uintptr_t>(d_data) & 3)) return HS_ERR_ALIGNMENT;
+  PatternParams pp;
+  int rc = make_pattern(h_offset, h_count, total_slots, cap, pp);
+  if (rc != HS_OK) return rc;
+  DevInfo di;
+  if ((rc = dev_info(di)) != HS_OK) return rc;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemsetAsync(d_sink, 0, 8, st);
+  if (e != cudaSuccess) return fold(e);
+  if (d_out256 && (e = cudaMemsetAsync(d_out256, 0, 2048, st)) != cudaSuccess) return fold(e);
+  if (n_bytes == 0) return HS_OK;
+  const size_t smem = (256 * 32 + 8 * size_t(total_slots)) * 4;
+  if (smem > (size_t)di.smem_optin) return HS_ERR_UNSUPPORTED;
+  if ((rc = set_smem(k_ablation, smem)) != HS_OK) return rc;
+  const int per_sm = std::max(1, int(di.smem_optin / (smem + 1024)));
+  const uint64_t want = (n_bytes + (64ull << 10) - 1) / (64ull << 10);
+  const int grid = int(std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(di.sms) * per_sm)));
+  k_ablation<<<grid, kSubThreads, smem, st>>>(d_data, n_bytes, stage, pp,
+                                               reinterpret_cast<unsigned long long*>(d_sink),
+                                               reinterpret_cast<unsigned long long*>(d_out256));
+  return fold(cudaGetLastError());
+}
+
+int hs_generate_device(int kind, uint64_t seed, int value, double mean, double sigma, uint64_t first,
+                       uint8_t* d_out, uint64_t n, void* stream) {
+  if (n == 0) return HS_OK;
+  if (!d_out) return HS_ERR_INVALID_ARG;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  DevInfo di;
+  int rc = dev_info(di);
+  if (rc != HS_OK) return rc;
+  const int grid = di.sms * 8;
+  switch (kind) {
+    case HS_GEN_UNIFORM: k_gen_uniform<<<grid, 256, 0, st>>>(seed, first, d_out, n); break;
+    case HS_GEN_SEQUENTIAL: k_gen_sequential<<<grid, 256, 0, st>>>(first, d_out, n); break;
+    case HS_GEN_CONSTANT:
+      if (value < 0 || value > 255) return HS_ERR_INVALID_ARG;
+      return fold(cudaMemsetAsync(d_out, value, n, st));
+    case HS_GEN_NORMAL:
+      if (!(sigma > 0)) return HS_ERR_INVALID_ARG;
+      k_gen_normal<<<grid, 256, 0, st>>>(seed, mean, sigma, first, d_out, n);
+      break;
+    default: return HS_ERR_INVALID_ARG;  // mixture consumes a data-dependent draw count: host only
+  }
+  return fold(cudaGetLastError());
+}
+
+}  // extern "C"

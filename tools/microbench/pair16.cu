@@ -1,0 +1,171 @@
+// u16 lane-private "pair" counters: word (lane, j) counts bins 2j and 2j+1 together.
+// Each hit of byte b on pair j = b >> 1 adds 1 + (b << 16):
+//   lo = c[2j] + c[2j+1]                (exact while < 2^16)
+//   hi = sum(b) mod 2^16 = 2j*lo + c[2j+1] (mod 2^16)
+//   => c[2j+1] = (hi - 2j*lo) mod 2^16, c[2j] = lo - c[2j+1]
+// 16 KB per warp instead of 32 KB -> twice the warps per SM.
+// build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -o p16 pair16.cu
+#include <cstdio>
+#include <cstdint>
+#include <vector>
+#include <algorithm>
+#include <cuda_runtime.h>
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s line %d\n", cudaGetErrorString(e), __LINE__); return 1; } } while (0)
+
+__device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void red_add(uint32_t a, uint32_t v) { asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(v)); }
+__device__ __forceinline__ void red_inc(uint32_t a) { asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(a)); }
+
+// MODE 0: u32 lane-private (256 rows x 32 KB/warp), MODE 1: u16 pair (128 rows, 16 KB/warp)
+// MODE 2: u16 pair, warp pairs share 32 KB-aligned regions of 256-B rows so PRMT builds the address
+template <int MODE, int U, int TH>
+__global__ void __launch_bounds__(TH, 1) k(const uint4* __restrict__ in, size_t nvec, unsigned long long* out, unsigned* base_probe) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const uint32_t sb = (uint32_t)__cvta_generic_to_shared(sm);
+  if (blockIdx.x == 0 && threadIdx.x == 0) base_probe[0] = sb;
+  constexpr uint32_t REGION = MODE == 0 ? 32768 : 16384;
+  const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t zbytes = MODE == 2 ? 227 * 1024 : nw * REGION;
+  for (uint32_t i = threadIdx.x; i < zbytes / 16; i += blockDim.x)
+    asm volatile("st.shared.v4.u32 [%0], {%1,%1,%1,%1};" ::"r"(sb + i * 16), "r"(0));
+  __syncthreads();
+  // MODE 2 layout: region r = warps 2r, 2r+1 at align32k(sb) + r*32K; row hb (256 B) = [even warp | odd warp]
+  const uint32_t rb = ((sb + 32767u) & ~32767u) + (warp >> 1) * 32768u;
+  const uint32_t tb = MODE == 2 ? rb + (warp & 1) * 128 + lane * 4 : sb + warp * REGION + lane * 4;
+  const uint32_t hib4 = ((rb >> 15) & 1) ? 0x80808080u : 0u;
+  size_t per = (nvec + gridDim.x - 1) / gridDim.x;
+  size_t beg = blockIdx.x * per, end = min(nvec, beg + per);
+  const size_t batch = (size_t)U * blockDim.x;
+  const size_t nfull = (end - beg) / batch;
+  uint4 A[U], B[U];
+  auto word = [&](uint32_t w) {
+    if (MODE == 0) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) red_inc(tb + (__byte_perm(w, 0, 0x4440 | q) << 7));
+    } else if (MODE == 2) {
+      const uint32_t h = ((w >> 1) & 0x7f7f7f7fu) | hib4;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        red_add(__byte_perm(h, tb, 0x7604 | (q << 4)), __byte_perm(w, 1u, 0x7054 | (q << 8)));
+    } else {
+      const uint32_t h = (w >> 1) & 0x7f7f7f7fu;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        red_add(tb + (__byte_perm(h, 0, 0x4440 | q) << 7), __byte_perm(w, 1u, 0x7054 | (q << 8)));
+    }
+  };
+  auto vec = [&](const uint4& v) { word(v.x); word(v.y); word(v.z); word(v.w); };
+  const uint4* vp = in + beg;
+  if (nfull) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) A[u] = ldg_stream(vp + u * blockDim.x + threadIdx.x);
+  }
+  for (size_t j = 0; j < nfull; j += 2) {
+    if (threadIdx.x == 0 && (j + 3) * batch < (end - beg))
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(vp + (j + 3) * batch), "r"((uint32_t)(min(2 * batch, (end - beg) - (j + 3) * batch) * 16)) : "memory");
+    if (j + 1 < nfull) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) B[u] = ldg_stream(vp + (j + 1) * batch + u * blockDim.x + threadIdx.x);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) vec(A[u]);
+    if (j + 1 >= nfull) break;
+    if (j + 2 < nfull) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) A[u] = ldg_stream(vp + (j + 2) * batch + u * blockDim.x + threadIdx.x);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) vec(B[u]);
+  }
+  for (size_t i = beg + nfull * batch + threadIdx.x; i < end; i += blockDim.x) vec(ldg_stream(in + i));
+  asm volatile("" ::: "memory");
+  __syncthreads();
+  // simple (slow) reduction: thread per bin
+  for (int b = threadIdx.x; b < 256; b += blockDim.x) {
+    unsigned long long s = 0;
+    for (int w = 0; w < nw; ++w)
+      for (int l = 0; l < 32; ++l) {
+        const uint32_t* reg = reinterpret_cast<const uint32_t*>(sm + w * REGION);
+        if (MODE == 0) s += reg[b * 32 + ((l + b) & 31)];
+        else {
+          const uint32_t j = b >> 1;
+          uint32_t x;
+          if (MODE == 2) {
+            const uint32_t a = ((sb + 32767u) & ~32767u) + (w >> 1) * 32768u + j * 256 + (w & 1) * 128 + ((l + b) & 31) * 4;
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(x) : "r"(a));
+          } else x = reg[j * 32 + ((l + b) & 31)];
+          const uint32_t lo = x & 0xffff, hi = x >> 16;
+          const uint32_t odd = (hi - 2 * j * lo) & 0xffff;
+          s += (b & 1) ? odd : lo - odd;
+        }
+      }
+    if (s) atomicAdd(out + b, s);
+  }
+}
+
+template <int MODE, int U, int TH>
+int run(const uint4* d, size_t n, unsigned long long* out, unsigned* probe, int sms, const std::vector<unsigned long long>& ref, const char* tag) {
+  size_t smem = MODE == 2 ? 227 * 1024 : (size_t)(TH / 32) * (MODE == 0 ? 32768 : 16384);
+  CK(cudaFuncSetAttribute(k<MODE, U, TH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  std::vector<float> t;
+  cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+  bool ok = true;
+  for (int r = 0; r < 8; ++r) {
+    cudaMemset(out, 0, 2048);
+    cudaEventRecord(a);
+    k<MODE, U, TH><<<sms, TH, smem>>>(d, n / 16, out, probe);
+    cudaEventRecord(b);
+    CK(cudaEventSynchronize(b));
+    float ms; cudaEventElapsedTime(&ms, a, b);
+    if (r >= 3) t.push_back(ms);
+    if (r == 0) {
+      std::vector<unsigned long long> h(256);
+      cudaMemcpy(h.data(), out, 2048, cudaMemcpyDeviceToHost);
+      ok = h == ref;
+    }
+  }
+  unsigned pb; cudaMemcpy(&pb, probe, 4, cudaMemcpyDeviceToHost);
+  std::sort(t.begin(), t.end());
+  printf("%-8s U=%d warps=%2d smem=%6zu sbase=0x%x  %.3f ms  %7.1f GB/s  %s\n", tag, U, TH / 32, smem, pb, t[2], n / (t[2] * 1e6), ok ? "exact" : "MISMATCH");
+  return 0;
+}
+
+__global__ void fill(uint8_t* p, size_t n, int kind) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n / 8; i += (size_t)gridDim.x * blockDim.x) {
+    uint64_t z = (i + 1) * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull; z = (z ^ (z >> 27)) * 0x94D049BB133111EBull; z ^= z >> 31;
+    reinterpret_cast<uint64_t*>(p)[i] = kind == 0 ? z : (kind == 1 ? 0x7f7f7f7f7f7f7f7full : (z & 0x0707070707070707ull) + 0x7c7c7c7c7c7c7c7cull);
+  }
+}
+
+int main() {
+  size_t n = (size_t)1 << 30;
+  uint8_t* d; CK(cudaMalloc(&d, n));
+  unsigned long long* out; CK(cudaMalloc(&out, 2048));
+  unsigned* probe; CK(cudaMalloc(&probe, 4));
+  int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  std::vector<uint8_t> h(n);
+  for (int kind = 0; kind < 3; ++kind) {
+    fill<<<sms * 8, 256>>>(d, n, kind);
+    CK(cudaDeviceSynchronize());
+    cudaMemcpy(h.data(), d, n, cudaMemcpyDeviceToHost);
+    std::vector<unsigned long long> ref(256, 0);
+    for (size_t i = 0; i < n; ++i) ref[h[i]]++;
+    printf("-- data kind %d (0 uniform, 1 const127, 2 narrow 124..131)\n", kind);
+    const uint4* in = reinterpret_cast<const uint4*>(d);
+    run<0, 8, 224>(in, n, out, probe, sms, ref, "u32");
+    run<1, 8, 384>(in, n, out, probe, sms, ref, "pair16");
+    run<1, 8, 448>(in, n, out, probe, sms, ref, "pair16");
+    run<2, 8, 384>(in, n, out, probe, sms, ref, "pair16p");
+    run<2, 6, 384>(in, n, out, probe, sms, ref, "pair16p");
+    run<2, 10, 384>(in, n, out, probe, sms, ref, "pair16p");
+    run<2, 8, 256>(in, n, out, probe, sms, ref, "pair16p");
+  }
+  return 0;
+}
