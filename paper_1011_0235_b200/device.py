@@ -1,0 +1,322 @@
+"""Device runtime around libhist256: staging, launches and readback.
+
+PyTorch is used only as plumbing — the CUDA caching allocator for device buffers,
+pinned host memory and streams/events. All counting happens in libhist256's sm_100a
+kernels through the C ABI (include/hist256.h); if CUDA or the library is missing
+every entry point raises (there is no CPU fallback).
+
+Data flow for one batch (the reference's batch_histograms, stream.py:260-316):
+  host PackedChunks --H2D (pinned: async; pageable: staged by the driver)--> one device
+  staging buffer -> hs_histogram_batched (one launch, one segment per chunk) ->
+  uint64[n, 256] on device --D2H 2 KiB per chunk--> read-only Histogram256 values.
+DeviceChunks skip the H2D: their tensors are segments of the same launch.
+"""
+from __future__ import annotations
+
+import bisect
+import threading
+import warnings
+import weakref
+from dataclasses import dataclass, field
+from typing import Sequence
+
+import numpy as np
+
+from . import _native as N
+from .core import BINS, DeviceChunk, PackedChunk
+
+_torch = None
+
+
+def torch():
+    """Import torch lazily (host-only helpers must not pay for it)."""
+    global _torch
+    if _torch is None:
+        import torch as t
+
+        _torch = t
+    return _torch
+
+
+class DeviceUnavailable(RuntimeError):
+    """No CUDA device: the histogram path runs only on the GPU (no CPU fallback)."""
+
+
+def require_cuda():
+    t = torch()
+    if not t.cuda.is_available():
+        raise DeviceUnavailable("CUDA device required: libhist256 has no CPU fallback")
+    N.lib()
+    return t
+
+
+# ------------------------------------------------------------------ pinned host memory
+class _PinnedRegistry:
+    """Address ranges of pinned buffers handed out by pinned_words()/pinned_bytes()."""
+
+    def __init__(self):
+        self._lock = threading.Lock()
+        self._starts: list[int] = []
+        self._ends: list[int] = []
+
+    def add(self, tensor) -> None:
+        start = tensor.data_ptr()
+        end = start + tensor.numel() * tensor.element_size()
+        with self._lock:
+            i = bisect.bisect_left(self._starts, start)
+            self._starts.insert(i, start)
+            self._ends.insert(i, end)
+        # the numpy view keeps the tensor alive; the range is dropped with it
+        weakref.finalize(tensor, self._drop, start)
+
+    def _drop(self, start: int) -> None:
+        with self._lock:
+            i = bisect.bisect_left(self._starts, start)
+            if i < len(self._starts) and self._starts[i] == start:
+                del self._starts[i]
+                del self._ends[i]
+
+    def contains(self, ptr: int, nbytes: int) -> bool:
+        with self._lock:
+            i = bisect.bisect_right(self._starts, ptr) - 1
+            return i >= 0 and ptr + nbytes <= self._ends[i]
+
+
+_pinned = _PinnedRegistry()
+
+
+def pinned_bytes(n: int) -> np.ndarray:
+    """A uint8 numpy array backed by page-locked host memory (async H2D source)."""
+    t = require_cuda().empty(max(int(n), 1), dtype=torch().uint8, pin_memory=True)
+    _pinned.add(t)
+    arr = t.numpy()[: int(n)]
+    return arr
+
+
+def pinned_words(n_words: int) -> np.ndarray:
+    """A uint32 numpy array backed by page-locked host memory."""
+    return pinned_bytes(4 * int(n_words)).view(np.uint32)
+
+
+def is_pinned(arr: np.ndarray) -> bool:
+    return _pinned.contains(arr.ctypes.data, arr.nbytes)
+
+
+# ------------------------------------------------------------------ staging
+class Staging:
+    """A growable device buffer (+ pinned readback buffer) owned by one stream user.
+
+    Reuse is safe once the work that read it has completed; the synchronous API
+    waits for its readback, the pipeline releases a slot only after its batch is
+    folded (stream.py:_StageBuffer protocol)."""
+
+    def __init__(self, device=None):
+        t = require_cuda()
+        self.device = t.device("cuda", t.cuda.current_device() if device is None else t.device(device).index)
+        self._dev = None
+        self._out_host = None
+
+    def device_bytes(self, n: int):
+        t = torch()
+        if self._dev is None or self._dev.numel() < n:
+            cap = max(n, 1 << 20)
+            self._dev = t.empty(cap + 256, dtype=t.uint8, device=self.device)
+        # 256-B aligned start (the allocator returns 512-B aligned blocks)
+        return self._dev
+
+    def host_out(self, nseg: int):
+        t = torch()
+        need = nseg * BINS
+        if self._out_host is None or self._out_host.numel() < need:
+            self._out_host = t.empty(max(need, 64 * BINS), dtype=t.int64, pin_memory=True)
+        return self._out_host[:need]
+
+
+@dataclass
+class StagedBatch:
+    """A batch whose bytes are on the device: segment s is [base+begin[s], base+end[s])."""
+
+    base: int
+    begin: np.ndarray
+    end: np.ndarray
+    keepalive: list = field(default_factory=list)
+    ready: object = None  # torch.cuda.Event recorded after the H2D copies, or None
+
+    @property
+    def nseg(self) -> int:
+        return int(self.begin.size)
+
+    @property
+    def nbytes(self) -> int:
+        return int((self.end - self.begin).sum())
+
+
+def stage(chunks: Sequence, staging: Staging | None, stream=None) -> StagedBatch:
+    """Place a batch on the device. Host chunks are copied (async when their memory is
+    pinned) into ``staging``'s buffer at word-aligned offsets on ``stream``; device
+    chunks are referenced in place. Records ``ready`` after the copies."""
+    t = require_cuda()
+    stream = stream or t.cuda.current_stream()
+    host = [(i, c) for i, c in enumerate(chunks) if isinstance(c, PackedChunk)]
+    ptrs = [0] * len(chunks)
+    sizes = [0] * len(chunks)
+    keep: list = []
+    ready = None
+    if host:
+        total = sum(c.byte_size for _, c in host)
+        if staging is None:
+            staging = Staging()
+        dev = staging.device_bytes(total)
+        keep.append(dev)
+        base = dev.data_ptr()
+        off = 0
+        with t.cuda.stream(stream):
+            for i, c in host:
+                n = c.byte_size
+                if n:
+                    with warnings.catch_warnings():  # chunks are read-only views; torch only reads them
+                        warnings.simplefilter("ignore", UserWarning)
+                        src = t.from_numpy(c.words.view(np.uint8))
+                    dev[off:off + n].copy_(src, non_blocking=True)
+                    keep.append(src)
+                ptrs[i] = base + off
+                sizes[i] = n
+                off += n
+            ready = t.cuda.Event()
+            ready.record(stream)
+    for i, c in enumerate(chunks):
+        if isinstance(c, DeviceChunk):
+            ptrs[i] = c.data.data_ptr()
+            sizes[i] = c.byte_size
+            keep.append(c.data)
+        elif not isinstance(c, PackedChunk):
+            raise TypeError(f"expected PackedChunk or DeviceChunk, got {type(c).__name__}")
+    nonempty = [p for p, s in zip(ptrs, sizes) if s]
+    base = min(nonempty) if nonempty else 0
+    begin = np.array([(p - base) if s else 0 for p, s in zip(ptrs, sizes)], dtype=np.uint64)
+    end = begin + np.array(sizes, dtype=np.uint64)
+    return StagedBatch(base, begin, end, keep, ready)
+
+
+def _pattern_args(pattern):
+    if pattern is None:
+        return None, None, 0, 0, None
+    off = np.ascontiguousarray(pattern.offset, dtype=np.int64)
+    cnt = np.ascontiguousarray(pattern.count, dtype=np.int64)
+    return N.i64p(off), N.i64p(cnt), int(pattern.total_slots), int(pattern.cap), (off, cnt)
+
+
+def launch(staged: StagedBatch, kind: int, pattern=None, stream=None, impl: int = N.HS_IMPL_AUTO, out=None):
+    """hs_histogram_batched on ``stream`` (waits for the staging copies first).
+    Returns the device int64 tensor [nseg, 256] (counts, reinterpret as uint64)."""
+    t = require_cuda()
+    stream = stream or t.cuda.current_stream()
+    if staged.ready is not None:
+        stream.wait_event(staged.ready)
+    nseg = staged.nseg
+    if out is None:
+        with t.cuda.stream(stream):
+            out = t.empty((max(nseg, 1), BINS), dtype=t.int64, device=t.cuda.current_device())
+    off_p, cnt_p, S, cap, keep = _pattern_args(pattern)
+    begin = np.ascontiguousarray(staged.begin, dtype=np.uint64)
+    end = np.ascontiguousarray(staged.end, dtype=np.uint64)
+    status = N.lib().hs_histogram_batched(
+        staged.base or None, N.u64p(begin), N.u64p(end), nseg, int(kind), int(impl),
+        off_p, cnt_p, S, cap, out.data_ptr(), None, 0, stream.cuda_stream)
+    N.check(status, "hs_histogram_batched")
+    return out[:nseg] if nseg else out[:0]
+
+
+def readback(out_dev, staging: Staging | None = None, stream=None) -> np.ndarray:
+    """D2H of [n, 256] counts (pinned, async) then wait; returns uint64 numpy (a copy)."""
+    t = torch()
+    stream = stream or t.cuda.current_stream()
+    n = out_dev.shape[0]
+    if n == 0:
+        return np.zeros((0, BINS), np.uint64)
+    host = staging.host_out(n) if staging is not None else t.empty(n * BINS, dtype=t.int64, pin_memory=True)
+    with t.cuda.stream(stream):
+        host.view(n, BINS).copy_(out_dev, non_blocking=True)
+        ev = t.cuda.Event()
+        ev.record(stream)
+    ev.synchronize()
+    return host.numpy().reshape(n, BINS).view(np.uint64).copy()
+
+
+_local = threading.local()
+
+
+def default_staging() -> Staging:
+    """Per-thread staging for the synchronous API (the reference's workers are called
+    from several Python threads concurrently, kernels.py:319-327)."""
+    s = getattr(_local, "staging", None)
+    t = require_cuda()
+    if s is None or s.device.index != t.cuda.current_device():
+        s = Staging()
+        _local.staging = s
+    return s
+
+
+def histograms(chunks: Sequence, kind: int, pattern=None, impl: int = N.HS_IMPL_AUTO) -> np.ndarray:
+    """Synchronous batched histograms of host/device chunks -> uint64 [n, 256]."""
+    t = require_cuda()
+    stream = t.cuda.current_stream()
+    st = default_staging()
+    staged = stage(chunks, st, stream)
+    out = launch(staged, kind, pattern, stream, impl)
+    return readback(out, st, stream)
+
+
+def histogram_tensor(data, kind: int = N.HS_KIND_NAIVE, pattern=None, impl: int = N.HS_IMPL_AUTO,
+                     stream=None, out=None):
+    """Histogram of a device-resident uint8 tensor; returns the device int64[256] without
+    synchronising (for device pipelines, multi-GPU reduction and benchmarks)."""
+    staged = stage([DeviceChunk(data)], None, stream)
+    return launch(staged, kind, pattern, stream, impl, out=out)[0]
+
+
+def group_slots(chunk, pattern, group_size: int, group_count: int, mode: int) -> np.ndarray:
+    """Reference-mapping slot totals (hs_group_slots): mode 0 u64[G,S], 1 u64[G,gs,S],
+    2 u16[G,S] wrapped."""
+    t = require_cuda()
+    stream = t.cuda.current_stream()
+    staged = stage([chunk], default_staging(), stream)
+    if staged.ready is not None:
+        stream.wait_event(staged.ready)
+    S = int(pattern.total_slots)
+    shape = (group_count, group_size, S) if mode == 1 else (group_count, S)
+    dtype = t.int16 if mode == 2 else t.int64
+    out = t.empty(shape, dtype=dtype, device=t.cuda.current_device())
+    off_p, cnt_p, S, cap, keep = _pattern_args(pattern)
+    base = staged.base + int(staged.begin[0]) if staged.nbytes else 0
+    status = N.lib().hs_group_slots(base or None, staged.nbytes, int(group_size), int(group_count),
+                                    off_p, cnt_p, S, cap, int(mode), out.data_ptr(), stream.cuda_stream)
+    N.check(status, "hs_group_slots")
+    host = out.cpu().numpy()
+    return host.view(np.uint16) if mode == 2 else host.view(np.uint64)
+
+
+def ablation_stage(chunk, stage_id: int, pattern):
+    """One genealogy stage (hs_ablation_stage), timed with CUDA events on the launch
+    stream. Returns (seconds, checksum, histogram-or-None)."""
+    t = require_cuda()
+    stream = t.cuda.current_stream()
+    staged = stage([chunk], default_staging(), stream)
+    if staged.ready is not None:
+        stream.wait_event(staged.ready)
+    sink = t.empty(1, dtype=t.int64, device=t.cuda.current_device())
+    out = t.empty(BINS, dtype=t.int64, device=t.cuda.current_device())
+    off_p, cnt_p, S, cap, keep = _pattern_args(pattern)
+    base = staged.base + int(staged.begin[0]) if staged.nbytes else 0
+    a = t.cuda.Event(enable_timing=True)
+    b = t.cuda.Event(enable_timing=True)
+    a.record(stream)
+    status = N.lib().hs_ablation_stage(base or None, staged.nbytes, int(stage_id), off_p, cnt_p, S, cap,
+                                       sink.data_ptr(), out.data_ptr(), None, 0, stream.cuda_stream)
+    b.record(stream)
+    N.check(status, "hs_ablation_stage")
+    b.synchronize()
+    seconds = a.elapsed_time(b) / 1e3
+    checksum = int(sink.cpu().numpy().view(np.uint64)[0])
+    hist = out.cpu().numpy().view(np.uint64).copy() if stage_id == N.HS_STAGE_FULL else None
+    return seconds, checksum, hist

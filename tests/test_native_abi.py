@@ -1,0 +1,86 @@
+"""The C-ABI library loads on a CPU box and exports every symbol include/hist256.h
+declares; argument validation that happens before any device call returns the
+documented status codes. No kernels are launched here."""
+import ctypes
+import re
+from pathlib import Path
+
+import numpy as np
+
+from paper_1011_0235_b200 import _native as N
+
+HEADER = Path(__file__).resolve().parents[1] / "include" / "hist256.h"
+
+
+def declared_functions():
+    text = re.sub(r"/\*.*?\*/", "", HEADER.read_text(), flags=re.S)
+    return sorted(set(re.findall(r"\b(hs_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_header_and_binding_agree():
+    assert declared_functions() == sorted(N.EXPORTED)
+
+
+def test_library_exports_every_declared_symbol():
+    lib = N.lib()
+    raw = ctypes.CDLL(str(N.library_path()))
+    for name in declared_functions():
+        assert hasattr(raw, name), name
+        assert getattr(lib, name) is not None
+
+
+def test_library_is_sm100a_only():
+    import subprocess
+
+    out = subprocess.run(["cuobjdump", "--list-elf", str(N.library_path())], capture_output=True, text=True)
+    if out.returncode == 0:
+        archs = set(re.findall(r"sm_(\d+a?)", out.stdout))
+        assert archs == {"100a"}, archs
+
+
+def test_status_strings():
+    lib = N.lib()
+    assert lib.hs_abi_version() == 1
+    assert lib.hs_strerror(N.HS_OK) == b"ok"
+    assert lib.hs_strerror(N.HS_ERR_PATTERN_COUNT_LOW) == b"count below 1"
+    assert lib.hs_strerror(N.HS_ERR_PATTERN_OFFSETS) == b"offsets not contiguous"
+
+
+def test_argument_validation_before_device_work():
+    lib = N.lib()
+    b = np.zeros(1, np.uint64)
+    e = np.full(1, 8, np.uint64)
+    # bad kind / impl / missing pattern for ADAPTIVE are rejected up front
+    assert lib.hs_histogram_batched(None, N.u64p(b), N.u64p(e), 1, 7, 0, None, None, 0, 0, None, None, 0, None) == N.HS_ERR_INVALID_ARG
+    assert lib.hs_histogram_batched(None, N.u64p(b), N.u64p(e), 1, 0, 9, None, None, 0, 0, None, None, 0, None) == N.HS_ERR_INVALID_ARG
+    out = ctypes.c_void_p(16)  # never dereferenced: validation fails first
+    assert lib.hs_histogram_batched(None, N.u64p(b), N.u64p(e), 1, N.HS_KIND_ADAPTIVE, 0, None, None, 960, 8, out, None, 0, None) == N.HS_ERR_INVALID_ARG
+    # misaligned segment bounds
+    e3 = np.full(1, 6, np.uint64)
+    assert lib.hs_histogram_batched(ctypes.c_void_p(256), N.u64p(b), N.u64p(e3), 1, 0, 0, None, None, 0, 0, out, None, 0, None) == N.HS_ERR_ALIGNMENT
+    # invalid patterns, in the reference's check order
+    off = np.arange(256, dtype=np.int64) * 3
+    cnt = np.full(256, 3, np.int64)
+    assert lib.hs_validate_pattern(N.i64p(off), N.i64p(cnt), 768, 8) == N.HS_OK
+    cnt[5] = 0
+    assert lib.hs_validate_pattern(N.i64p(off), N.i64p(cnt), 768, 8) == N.HS_ERR_PATTERN_COUNT_LOW
+    cnt[5] = 9
+    assert lib.hs_validate_pattern(N.i64p(off), N.i64p(cnt), 768, 8) == N.HS_ERR_PATTERN_COUNT_HIGH
+    cnt[5] = 3
+    assert lib.hs_validate_pattern(N.i64p(off), N.i64p(cnt), 767, 8) == N.HS_ERR_PATTERN_TOTAL
+    off[7] += 1
+    assert lib.hs_validate_pattern(N.i64p(off), N.i64p(cnt), 768, 8) == N.HS_ERR_PATTERN_OFFSETS
+    prior = np.zeros(256, np.uint64)
+    o2, c2 = np.zeros(256, np.int64), np.zeros(256, np.int64)
+    assert lib.hs_binning_pattern(N.u64p(prior), 255, 8, N.i64p(o2), N.i64p(c2)) == N.HS_ERR_SLOT_RANGE
+    assert lib.hs_binning_pattern(N.u64p(prior), 960, 0, N.i64p(o2), N.i64p(c2)) == N.HS_ERR_SLOT_RANGE
+
+
+def test_missing_library_fails_loudly(monkeypatch, tmp_path):
+    import pytest
+
+    monkeypatch.setattr(N, "_lib", None)
+    monkeypatch.setenv("HS_LIBHIST256", str(tmp_path / "nope.so"))
+    with pytest.raises(N.NativeLibraryError):
+        N.lib()
+    monkeypatch.setattr(N, "_lib", None)
