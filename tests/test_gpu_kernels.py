@@ -1,0 +1,284 @@
+"""GPU parity of the histogram kernels through the drop-in API (and the C ABI under
+it) against the oracle and reference-generated vectors. Bit-exact integer results.
+
+Mirrors the reference's kernel tests (test_kernels.py) and acceptance c01
+(test_acceptance.py:56-91), plus every device strategy (HS_IMPL_*), unaligned and
+ragged device segments, and the slot-level compat outputs."""
+import zlib
+
+import numpy as np
+import pytest
+
+import paper_1011_0235_b200 as hs
+from paper_1011_0235_b200 import _native as N
+from paper_1011_0235_b200 import device as D
+
+pytestmark = pytest.mark.gpu
+
+IMPLS = [N.HS_IMPL_AUTO, N.HS_IMPL_LANE, N.HS_IMPL_WARP, N.HS_IMPL_SUBBIN]
+
+
+def chunk_of(oracle, kind, pixels, seed=0, **kw):
+    return hs.PackedChunk(oracle.pack(oracle.generate(kind, pixels, seed, **kw)))
+
+
+def deg_pattern(value=127, slots=960, cap=8):
+    c = np.zeros(256, np.uint64)
+    c[value] = 1_000_000
+    return hs.compute_binning_pattern(hs.Histogram256(c), slots, cap)
+
+
+def test_hand_count_and_empty(cuda):
+    cfg = hs.WorkerGroupConfig(8, 3)
+    h = hs.naive_histogram(hs.pack_pixels([1, 1, 2, 0]), cfg)
+    assert h.counts[0] == 1 and h.counts[1] == 2 and h.counts[2] == 1 and h.total() == 4
+    assert hs.naive_histogram(hs.pack_pixels([]), cfg).total() == 0
+    assert hs.adaptive_histogram(hs.pack_pixels([]), hs.uniform_pattern(960), cfg).total() == 0
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_randomized_triples(cuda, oracle, seed):
+    # test_kernels.py:97-115
+    rng = np.random.default_rng(900 + seed)
+    pixels = int(rng.integers(1, 1 << 12)) * 4
+    kind = str(rng.choice(["uniform", "mixture", "constant", "sequential", "normal"]))
+    px = oracle.generate(kind, pixels, int(rng.integers(0, 2**32)), value=int(rng.integers(0, 256)),
+                         degeneracy=float(rng.uniform(0, 1)), mean=float(rng.uniform(0, 255)),
+                         sigma=float(rng.uniform(1, 80)))
+    chunk = hs.PackedChunk(oracle.pack(px))
+    cfg = hs.WorkerGroupConfig(int(rng.integers(1, 9)), int(rng.integers(1, 5)))
+    cap = int(rng.integers(1, 9))
+    slots = int(rng.integers(256, 256 * cap + 1))
+    pattern = hs.compute_binning_pattern(hs.Histogram256(rng.integers(0, 1 << 16, 256).astype(np.uint64)), slots, cap)
+    want = oracle.histogram(px)
+    assert np.array_equal(hs.naive_histogram(chunk, cfg).counts, want)
+    assert np.array_equal(hs.adaptive_histogram(chunk, pattern, cfg).counts, want)
+    for impl in IMPLS:
+        kindid = N.HS_KIND_ADAPTIVE if impl != N.HS_IMPL_WARP else N.HS_KIND_NAIVE
+        assert np.array_equal(D.histograms([chunk], kindid, pattern, impl)[0], want), impl
+
+
+@pytest.mark.parametrize("kind", ["uniform", "normal", "constant", "sequential", "mixture"])
+@pytest.mark.parametrize("impl", IMPLS)
+def test_sizes_and_impls(cuda, oracle, kind, impl):
+    rng = np.random.default_rng(zlib.crc32(f"{kind}/{impl}".encode()))
+    for pixels in (4, 60, 4096, (1 << 20) + 20, (9 << 20) + 4):  # below/above the AUTO switch at 8 MiB
+        px = oracle.generate(kind, pixels, int(rng.integers(0, 2**40)), value=200, mean=128.0, sigma=8.0,
+                             degeneracy=0.7)
+        pat = hs.compute_binning_pattern(hs.Histogram256(oracle.histogram(px)))
+        for k in (N.HS_KIND_NAIVE, N.HS_KIND_ADAPTIVE):
+            got = D.histograms([hs.PackedChunk(oracle.pack(px))], k, pat, impl)[0]
+            assert np.array_equal(got, oracle.histogram(px)), (kind, impl, pixels, k)
+
+
+def test_device_chunks_unaligned_and_ragged(cuda, oracle):
+    torch = cuda
+    px = oracle.generate("normal", (3 << 20) + 64, 5, mean=100.0, sigma=40.0)
+    dev = torch.from_numpy(px).cuda()
+    rng = np.random.default_rng(3)
+    for _ in range(20):
+        a = int(rng.integers(0, px.size // 4)) * 4
+        b = int(rng.integers(a // 4, px.size // 4 + 1)) * 4
+        for impl in IMPLS:
+            pat = hs.uniform_pattern(960)
+            got = D.histograms([hs.DeviceChunk(dev[a:b])], N.HS_KIND_ADAPTIVE, pat, impl)[0]
+            assert np.array_equal(got, oracle.histogram(px[a:b])), (a, b, impl)
+
+
+def test_batched_segments_mixed_host_device(cuda, oracle):
+    torch = cuda
+    rng = np.random.default_rng(7)
+    base = oracle.generate("mixture", 1 << 20, 11, value=77, degeneracy=0.4)
+    dev = torch.from_numpy(base).cuda()
+    cuts = sorted(int(x) * 4 for x in rng.integers(0, base.size // 4 + 1, 140))  # > kMaxSeg -> several launches
+    bounds = [0, *cuts, base.size]
+    slices = []
+    for i, (a, b) in enumerate(zip(bounds, bounds[1:])):
+        slices.append(hs.DeviceChunk(dev[a:b]) if i % 3 == 0 else hs.PackedChunk(oracle.pack(base[a:b])))
+    for kind, pattern in ((hs.KernelKind.NAIVE, None), (hs.KernelKind.ADAPTIVE, hs.uniform_pattern(960))):
+        got = hs.batch_histograms(slices, kind, pattern, hs.WorkerGroupConfig(4, 2))
+        assert [g.counts.tolist() for g in got] == [oracle.histogram(base[a:b]).tolist() for a, b in zip(bounds, bounds[1:])]
+        assert hs.merge_all(got).counts.tolist() == oracle.histogram(base).tolist()
+
+
+def test_batch_matches_reference_vectors(cuda, golden):
+    for i, m in enumerate(golden.meta["batches"]):
+        px = golden[f"batch_{i}_pixels"]
+        words = px.view(np.uint32)
+        b = m["bounds"]
+        slices = [hs.PackedChunk(words[x:y]) for x, y in zip(b, b[1:])]
+        got = hs.batch_histograms(slices, hs.KernelKind(m["kind"]), hs.uniform_pattern(960), hs.WorkerGroupConfig(4, 2))
+        assert np.array_equal(np.stack([g.counts for g in got]), golden[f"batch_{i}_hists"])
+
+
+def test_batch_errors(cuda):
+    chunk = hs.generate(hs.SourceSpec("uniform", 64, 0))
+    cfg = hs.WorkerGroupConfig(8, 2)
+    with pytest.raises(ValueError):
+        hs.batch_histograms([], hs.KernelKind.NAIVE, None, cfg)
+    with pytest.raises(ValueError):
+        hs.batch_histograms([chunk], hs.KernelKind.ADAPTIVE, None, cfg)
+    with pytest.raises(ValueError):
+        hs.batch_histograms([chunk], hs.KernelKind.COPY_ONLY, None, cfg)
+
+
+def test_constant_maximal_contention(cuda, oracle):
+    # test_kernels.py:75-81 at GPU scale: every lane of every warp on one bin
+    for value in (127, 0, 255):
+        chunk = hs.PackedChunk(oracle.pack(np.full(64 << 20, value, np.uint8)))
+        cfg = hs.WorkerGroupConfig(32, 2)
+        h = hs.naive_histogram(chunk, cfg)
+        assert h.counts[value] == 64 << 20 and h.total() == 64 << 20
+        assert hs.adaptive_histogram(chunk, deg_pattern(value), cfg) == h
+        # hot bin differing from the data's value exercises the non-hot path
+        assert hs.adaptive_histogram(chunk, deg_pattern((value + 1) % 256), cfg) == h
+
+
+def test_slots_match_reference(cuda, golden, oracle):
+    for i, m in enumerate(golden.meta["slots"]):
+        px = golden[f"slots_{i}_pixels"]
+        chunk = hs.PackedChunk(px.view(np.uint32))
+        pattern = hs.BinningPattern(golden[f"slots_{i}_offset"], golden[f"slots_{i}_count"], m["total_slots"], m["cap"])
+        cfg = hs.WorkerGroupConfig(m["group_size"], m["group_count"])
+        hist, slots = hs.adaptive_histogram(chunk, pattern, cfg, return_slots=True)
+        assert np.array_equal(np.stack(slots), golden[f"slots_{i}_slots"])
+        assert np.array_equal(hist.counts, golden[f"slots_{i}_hist"])
+
+
+def test_lane_touches_match_reference(cuda, golden):
+    m = golden.meta["touch"]
+    chunk = hs.PackedChunk(golden["touch_pixels"].view(np.uint32))
+    c = golden["touch_count"]
+    pattern = hs.BinningPattern(golden["touch_offset"], c, int(c.sum()), 8)
+    result, touches = hs.adaptive_lane_touches(chunk, pattern, hs.WorkerGroupConfig(m["group_size"], m["group_count"]))
+    assert np.array_equal(np.stack(touches), golden["touch_out"])
+    assert result == hs.reference_histogram(chunk)
+
+
+def test_eight_subbin_spread_and_remainder(cuda):
+    # test_kernels.py:140-165
+    chunk = hs.generate(hs.SourceSpec("constant", 1 << 16, 0, value=127))
+    pattern = deg_pattern(127)
+    result, gs = hs.adaptive_histogram(chunk, pattern, hs.WorkerGroupConfig(32, 2), return_slots=True)
+    comb = np.sum(gs, axis=0)
+    span = slice(int(pattern.offset[127]), int(pattern.offset[127]) + 8)
+    assert (comb[span] == (1 << 16) // 8).all() and comb.sum() == 1 << 16
+    pixels = (1 << 16) + 12
+    chunk = hs.generate(hs.SourceSpec("constant", pixels, 0, value=127))
+    _, gs = hs.adaptive_histogram(chunk, pattern, hs.WorkerGroupConfig(32, 2), return_slots=True)
+    hot = np.sum(gs, axis=0)
+    hot = hot[hot > 0]
+    assert len(hot) == 8 and (np.abs(hot.astype(np.int64) - pixels / 8) <= 4 * 32 * 2).all()
+
+
+def test_narrow_counters(cuda, golden):
+    chunk = hs.PackedChunk(golden["narrow_pixels"].view(np.uint32))
+    got, slots = hs.adaptive_histogram(chunk, hs.uniform_pattern(960), hs.WorkerGroupConfig(8, 2),
+                                       narrow_counters=True, return_slots=True)
+    assert np.array_equal(np.stack(slots), golden["narrow_slots"])
+    assert got == hs.reference_histogram(chunk)
+    big = hs.generate(hs.SourceSpec("constant", 1 << 20, 0, value=127))
+    with pytest.raises(hs.SubCounterOverflow):
+        hs.adaptive_histogram(big, deg_pattern(127), hs.WorkerGroupConfig(32, 1), narrow_counters=True)
+
+
+def test_slot_simulation_random(cuda, oracle):
+    # test_kernels.py:167-182 with the numpy simulation as oracle
+    rng = np.random.default_rng(31)
+    for _ in range(8):
+        px = oracle.generate("mixture", int(rng.integers(1, 2000)) * 4, int(rng.integers(0, 1 << 32)),
+                             value=int(rng.integers(0, 256)), degeneracy=float(rng.uniform(0, 1)))
+        words = oracle.pack(px)
+        cfg = hs.WorkerGroupConfig(int(rng.integers(1, 12)), int(rng.integers(1, 4)))
+        pattern = hs.compute_binning_pattern(hs.Histogram256(rng.integers(0, 1000, 256).astype(np.uint64)))
+        _, slots = hs.adaptive_histogram(hs.PackedChunk(words), pattern, cfg, return_slots=True)
+        want = oracle.simulate_slots(words, pattern.offset, pattern.count, 960, cfg.group_size, cfg.group_count)
+        for g, w in zip(slots, want):
+            assert np.array_equal(g, w)
+
+
+def test_dispatch_and_pattern_errors(cuda):
+    chunk = hs.generate(hs.SourceSpec("uniform", 256, seed=1))
+    cfg = hs.WorkerGroupConfig(4, 1)
+    want = hs.reference_histogram(chunk)
+    assert hs.compute_histogram(chunk, hs.KernelKind.NAIVE, None, cfg) == want
+    assert hs.compute_histogram(chunk, hs.KernelKind.ADAPTIVE, hs.uniform_pattern(960), cfg) == want
+    with pytest.raises(ValueError):
+        hs.compute_histogram(chunk, hs.KernelKind.ADAPTIVE, None, cfg)
+    with pytest.raises(ValueError):
+        hs.compute_histogram(chunk, hs.KernelKind.COPY_ONLY, None, cfg)
+    base = hs.uniform_pattern(960)
+    counts = base.count.copy()
+    counts[0] = 0
+    with pytest.raises(hs.InvalidPattern):
+        hs.adaptive_histogram(chunk, hs.BinningPattern(base.offset, counts, 960, 8), cfg)
+
+
+def test_reduce_subbins(cuda):
+    p = hs.uniform_pattern(960)
+    slots = np.zeros(960, np.uint64)
+    slots[int(p.offset[5]):int(p.offset[5]) + 3] = [2, 3, 4]
+    assert hs.reduce_subbins(slots, p).counts[5] == 9
+    with pytest.raises(ValueError):
+        hs.reduce_subbins(np.zeros(959, np.uint64), p)
+
+
+def test_ablation_stages(cuda):
+    chunk = hs.generate(hs.SourceSpec("uniform", 1 << 22, seed=13))
+    pattern = hs.compute_binning_pattern(hs.reference_histogram(chunk))
+    cfg = hs.WorkerGroupConfig(32, 2)
+    full = hs.run_ablation(chunk, hs.KernelKind.FULL, pattern, cfg)
+    assert full.histogram == hs.reference_histogram(chunk) and full.throughput_bps > 0
+    for stage in hs.ABLATION_STAGES:
+        a = hs.run_ablation(chunk, stage, pattern, cfg)
+        b = hs.run_ablation(chunk, stage, pattern, cfg)
+        assert a.checksum == b.checksum
+    sub = hs.run_ablation(chunk, hs.KernelKind.SUBHIST_NOREDUCE, pattern, cfg)
+    assert sub.checksum == chunk.pixel_count  # sum of every slot
+    with pytest.raises(ValueError):
+        hs.run_ablation(chunk, hs.KernelKind.NAIVE, pattern, cfg)
+
+
+def test_scheduling_independent(cuda):
+    chunk = hs.generate(hs.SourceSpec("mixture", 1 << 14, seed=6, value=127, degeneracy=0.7))
+    cfg = hs.WorkerGroupConfig(32, 4)
+    runs = [hs.naive_histogram(chunk, cfg) for _ in range(5)] + [hs.adaptive_histogram(chunk, deg_pattern(), cfg) for _ in range(5)]
+    assert all(r == runs[0] for r in runs)
+    s1 = hs.adaptive_histogram(chunk, deg_pattern(), cfg, return_slots=True)[1]
+    s2 = hs.adaptive_histogram(chunk, deg_pattern(), cfg, return_slots=True)[1]
+    assert all((a == b).all() for a, b in zip(s1, s2))
+
+
+def test_device_generators_match_host(cuda, oracle):
+    torch = cuda
+    for spec in (hs.SourceSpec("uniform", 1 << 20, 0xABC), hs.SourceSpec("normal", (1 << 18) + 4, 5, mean=128.0, sigma=8.0),
+                 hs.SourceSpec("sequential", 1000), hs.SourceSpec("constant", 4096, value=9)):
+        want = hs.unpack_chunk(hs.generate(spec))
+        for first in (0, 12, 4100):
+            n = spec.pixels - first if first < spec.pixels else 0
+            buf = torch.empty(n, dtype=torch.uint8, device="cuda")
+            hs.generate_device(spec, buf, first)
+            assert np.array_equal(buf.cpu().numpy(), want[first:]), (spec.kind, first)
+
+
+def test_concurrent_threads(cuda, oracle):
+    import threading
+
+    px = oracle.generate("uniform", 1 << 20, 42)
+    chunk = hs.PackedChunk(oracle.pack(px))
+    want = oracle.histogram(px)
+    errors = []
+
+    def work():
+        try:
+            for _ in range(5):
+                assert np.array_equal(hs.naive_histogram(chunk, hs.WorkerGroupConfig()).counts, want)
+        except BaseException as e:  # pragma: no cover
+            errors.append(e)
+
+    th = [threading.Thread(target=work) for _ in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors

@@ -1,0 +1,167 @@
+"""GPU streaming engine: run_pipeline == run_sequential, both == the reference's own
+run_sequential output (golden streams), double-buffer protocol order, switching
+latency and pipeline timing arithmetic. Mirrors test_stream.py and acceptance
+c06/c07/c09/c10 (test_acceptance.py:201-314)."""
+import io
+
+import numpy as np
+import pytest
+
+import paper_1011_0235_b200 as hs
+from paper_1011_0235_b200.datagen import batch_stream, schedule_stream
+
+pytestmark = pytest.mark.gpu
+
+SMALL = hs.WorkerGroupConfig(group_size=8, group_count=2)
+POLICY = hs.SwitchPolicy()
+
+
+def small_cfg(**kw):
+    base = dict(num_iterations=8, chunk_pixels=512, window_size=4, worker=SMALL)
+    base.update(kw)
+    return hs.PipelineConfig(**base)
+
+
+def uniform_source(cfg, seed=0):
+    return batch_stream(hs.SourceSpec("uniform", cfg.chunk_pixels, seed), cfg.num_iterations, cfg.batch_size)
+
+
+def states_equal(a, b):
+    return (a[0] == b[0] and a[1] == b[1] and a[3] == b[3]
+            and a[2].per_slice_histograms == b[2].per_slice_histograms
+            and a[2].degeneracy_log == b[2].degeneracy_log and a[2].divergence_log == b[2].divergence_log)
+
+
+def _segments(meta):
+    return [(hs.SourceSpec(s["kind"], s["pixels"], s["seed"], s["value"], s["mean"], s["sigma"], s["degeneracy"]), n)
+            for s, n in meta["segments"]]
+
+
+def test_streams_match_reference(cuda, golden):
+    for i, m in enumerate(golden.meta["streams"]):
+        cfg = hs.PipelineConfig(num_iterations=m["num_iterations"], chunk_pixels=m["chunk_pixels"],
+                                batch_size=m["batch_size"], recompute_pattern_every=m["recompute_pattern_every"],
+                                window_size=m["window_size"], worker=hs.WorkerGroupConfig(4, 2))
+        for runner in (hs.run_sequential, hs.run_pipeline):
+            acc, win, rep, log = runner(schedule_stream(_segments(m), m["batch_size"]), cfg, POLICY)
+            assert [k.value for k in log] == m["kernel_log"], (i, runner.__name__)
+            per = np.stack([np.stack([h.counts for h in it]) for it in rep.per_slice_histograms])
+            assert np.array_equal(per, golden[f"stream_{i}_per_slice"])
+            assert np.array_equal(acc.running.counts, golden[f"stream_{i}_acc"]) and acc.chunks_seen == m["chunks_seen"]
+            assert np.array_equal(win.windowed.counts, golden[f"stream_{i}_window"])
+            assert np.array_equal(np.stack([h.counts for h in win.ring]), golden[f"stream_{i}_ring"])
+            assert rep.degeneracy_log == golden[f"stream_{i}_deg"].tolist()
+            assert rep.divergence_log == golden[f"stream_{i}_div"].tolist()
+
+
+def test_pipeline_equals_sequential_batched(cuda):
+    cfg = small_cfg(batch_size=3, num_iterations=5)
+    seq = hs.run_sequential(uniform_source(cfg, 8), cfg, POLICY)
+    pipe = hs.run_pipeline(uniform_source(cfg, 8), cfg, POLICY)
+    assert states_equal(seq, pipe) and seq[0].chunks_seen == 15
+
+
+def test_degeneracy_flip(cuda):
+    cfg = small_cfg(num_iterations=12, window_size=2)
+    segs = [(hs.SourceSpec("uniform", cfg.chunk_pixels, 1), 6), (hs.SourceSpec("constant", cfg.chunk_pixels, 1, value=127), 6)]
+    seq = hs.run_sequential(schedule_stream(segs), cfg, POLICY)
+    pipe = hs.run_pipeline(schedule_stream(segs), cfg, POLICY)
+    assert states_equal(seq, pipe) and hs.KernelKind.ADAPTIVE in pipe[3]
+
+
+@pytest.mark.parametrize("every", [1, 3])
+def test_switch_latency(cuda, every):
+    # c10 (test_acceptance.py:292-314)
+    pixels, change = 2048, 100
+    segs = [(hs.SourceSpec("uniform", pixels, seed=10), change), (hs.SourceSpec("constant", pixels, seed=10, value=127), change)]
+    cfg = hs.PipelineConfig(num_iterations=2 * change, chunk_pixels=pixels, window_size=2,
+                            recompute_pattern_every=every, worker=hs.WorkerGroupConfig(4, 2))
+    _, _, _, log = hs.run_pipeline(schedule_stream(segs), cfg, hs.SwitchPolicy(0.45))
+    assert all(k is hs.KernelKind.NAIVE for k in log[:change + 1])
+    flip = next(i for i, k in enumerate(log) if k is hs.KernelKind.ADAPTIVE)
+    assert flip <= change + every + 1
+    assert all(k is hs.KernelKind.ADAPTIVE for k in log[flip:])
+
+
+def test_source_exhausted_and_errors(cuda):
+    cfg = small_cfg(num_iterations=10)
+    for runner in (hs.run_sequential, hs.run_pipeline):
+        with pytest.raises(hs.SourceExhausted):
+            runner(uniform_source(small_cfg(num_iterations=3), 1), cfg, POLICY)
+
+    def broken():
+        yield [hs.generate(hs.SourceSpec("uniform", 512, 0))]
+        raise RuntimeError("source failure")
+
+    with pytest.raises(RuntimeError, match="source failure"):
+        hs.run_pipeline(broken(), small_cfg(num_iterations=3), POLICY)
+
+
+def test_buffer_protocol_order(cuda):
+    cfg = small_cfg(num_iterations=9)
+    events = []
+    hs.run_pipeline(uniform_source(cfg, 9), cfg, POLICY, instrument=events)
+    for b in (0, 1):
+        mine = [(ev, it) for buf, ev, it in events if buf == b]
+        want = []
+        for it in range(b, 9, 2):
+            want += [("acquire_write", it), ("publish", it), ("take", it), ("release", it)]
+        assert mine == want
+    pos = {e: i for i, e in enumerate(events)}
+    for b, ev, it in events:
+        if ev == "acquire_write" and it >= 2:
+            assert pos[(b, "release", it - 2)] < pos[(b, ev, it)]
+
+
+def test_timing_structure(cuda):
+    cfg = small_cfg()
+    _, _, report, _ = hs.run_sequential(uniform_source(cfg, 2), cfg, POLICY)
+    assert report.total_sequential_ns == report.total_pipelined_ns and report.pipelined_ratio == 1.0
+    profile = hs.StageProfile(cpu_pre_us=1000, transfer_in_us=800, compute_us=3000, transfer_out_us=10)
+    ratios = {}
+    for n in (1, 8):
+        cfg = small_cfg(num_iterations=n, stage_profile=profile)
+        _, _, rep, _ = hs.run_pipeline(uniform_source(cfg, 4), cfg, POLICY)
+        assert rep.total_pipelined_ns <= rep.total_sequential_ns
+        ratios[n] = rep.pipelined_ratio
+    assert ratios[8] < ratios[1]
+
+
+def test_table3_pipeline_arithmetic(cuda):
+    # c06 (test_acceptance.py:201-210): Table 3 stage shares, 256 iterations
+    prof = hs.StageProfile(cpu_pre_us=2028.0, transfer_in_us=1768.0, compute_us=6201.0, transfer_out_us=2.0)
+    cfg = hs.PipelineConfig(num_iterations=256, chunk_pixels=1024, window_size=8, worker=hs.WorkerGroupConfig(4, 2),
+                            stage_profile=prof)
+    _, _, rep, _ = hs.run_pipeline(batch_stream(hs.SourceSpec("uniform", 1024, 606), 256), cfg, POLICY)
+    assert 0.60 <= rep.pipelined_ratio <= 0.68
+
+
+def test_csv_schema(cuda):
+    cfg = small_cfg(num_iterations=3)
+    _, _, report, _ = hs.run_sequential(uniform_source(cfg, 11), cfg, POLICY)
+    buf = io.StringIO()
+    report.to_csv(buf)
+    lines = buf.getvalue().strip().splitlines()
+    assert lines[0] == "iteration,cpu_pre_us,transfer_in_us,compute_us,transfer_out_us,cpu_post_us,kernel_kind"
+    assert len(lines) == 5 and lines[1].startswith("0,") and lines[1].endswith(",naive")
+    assert abs(float(lines[-1].split(",")[3]) - 100.0) < 1.0
+
+
+def test_device_resident_stream(cuda, oracle):
+    torch = cuda
+    # chunks already in HBM (the C2 configuration's device-resident form)
+    n_chunks, px = 8, 1 << 20
+    dev = torch.empty(n_chunks * px, dtype=torch.uint8, device="cuda")
+    spec = hs.SourceSpec("normal", px, 77, mean=128.0, sigma=32.0)
+    for i in range(n_chunks):
+        hs.generate_device(hs.SourceSpec("normal", px, 77 ^ i, mean=128.0, sigma=32.0), dev[i * px:(i + 1) * px])
+
+    def src():
+        for i in range(n_chunks):
+            yield [hs.DeviceChunk(dev[i * px:(i + 1) * px])]
+
+    cfg = hs.PipelineConfig(num_iterations=n_chunks, chunk_pixels=px, window_size=4)
+    acc, _, rep, log = hs.run_pipeline(src(), cfg, POLICY)
+    want = [oracle.histogram(oracle.generate("normal", px, 77 ^ i, mean=128.0, sigma=32.0)) for i in range(n_chunks)]
+    assert [h[0].counts.tolist() for h in rep.per_slice_histograms] == [w.tolist() for w in want]
+    assert acc.running.counts.tolist() == np.sum(want, axis=0).tolist()
