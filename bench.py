@@ -1,0 +1,421 @@
+#!/usr/bin/env python
+"""Benchmark of the 256-bin histogram hot path (BASELINE.json metric: input GB/s).
+
+Workload (BASELINE.json configs[1]): X-ray-like normal uint8 streams, mean 128,
+sigma 8 / 32 / 64, each 1 GiB as 64 chunks of 16 MiB (chunk seed = base ^ index,
+datagen.py:196-198), counted per chunk by the AHist path (HS_KIND_ADAPTIVE) with a
+CPU-computed binning pattern. One step = all three streams = 3 GiB = 192 per-chunk
+histograms in 3 batched launches. Inputs are generated in HBM once (bit-exact with
+the reference generator) and are 24x the 126 MB L2, so no flush is needed.
+
+The pattern for a stream's next step is computed on the host from that stream's
+previous per-chunk histograms while the other two streams' kernels run (the
+latency-hidden lag-1 switch/pattern of the paper, stream.py:14-20).
+
+  value   device-resident GB/s, CUDA events, max over ranks
+  e2e     same metric through the public streaming API (run_pipeline) with pinned
+          HOST buffers: H2D of every chunk and D2H of every result in the timed region
+  roofline  the ADAPTIVE kernel's achieved GB/s per launch vs MEASURED_PEAKS hbm_gbs
+  cpu_baseline  the oracle's restatement of the reference CPU path (arbitration-loop
+          adaptive worker, all host cores) on a bounded sample of the same stream
+
+Multi-GPU (torchrun): each rank owns the next 3 GiB of the stream (weak scaling);
+each step ends with one NCCL all_reduce of the step's 256 counts.
+``--impl reference`` times the oracle port only (rank 0) with the same metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+GiB = 1 << 30
+CHUNK = 16 << 20
+SIGMAS = (8.0, 32.0, 64.0)
+MEAN = 128.0
+BASE_SEED = 0x1011_0235
+METRIC = "256-bin histogram input GB/s at 1/2/4/8 B200 vs HBM roofline; CPU ref GB/s"
+WORKLOAD = "xray-normal-stream: 3 x 1 GiB (sigma 8/32/64, mean 128) in 16 MiB chunks, AHist + CPU pattern"
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+# ----------------------------------------------------------------------- clocks
+class ClockSampler:
+    """NVML SM clock + throttle reasons sampled every 5 ms during the timed region."""
+
+    BAD = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20}
+    NAMES = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+             0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+             0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index: int):
+        self.samples: list[int] = []
+        self.reasons = 0
+        self.max_mhz = None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # pragma: no cover - NVML missing
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self.nv is not None:
+            self._t.join()
+
+    def summary(self):
+        if self.nv is None or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        reasons = [n for bit, n in self.NAMES.items() if self.reasons & bit and bit != 0x1]
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------- distributed
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ----------------------------------------------------------------------- CPU baseline (oracle port)
+def cpu_baseline(streams, seconds: float = 10.0):
+    """The oracle's restatement of the reference's CPU AHist path (kernels.py:349-384:
+    arbitration-loop adaptive worker, one group thread per host core) on the bench
+    stream's own chunks (copied from HBM), until ~``seconds`` of CPU work."""
+    from oracle import oracle as O
+
+    cores = host_cores()
+    done_bytes, elapsed, chunks = 0, 0.0, 0
+    prior = [0] * 256
+    for i in range(64 * len(streams)):
+        j, c = i % len(streams), i // len(streams)
+        px = streams[j][c * CHUNK:(c + 1) * CHUNK].cpu().numpy()
+        off, cnt = O.binning_pattern(prior, 960, 8)
+        words = O.pack(px)
+        t0 = time.perf_counter()
+        hist, _, _ = O.adaptive_histogram(words, off, cnt, 960, 32, cores)
+        elapsed += time.perf_counter() - t0
+        prior = hist.tolist()
+        done_bytes += px.size
+        chunks += 1
+        if elapsed >= seconds:
+            break
+    return {"value": round(done_bytes / elapsed / 1e9, 4), "unit": "GB/s", "cores": cores, "kind": "port",
+            "sample": f"{chunks} x 16 MiB chunks of the sigma 8/32/64 normal streams "
+                      f"({done_bytes / GiB:.2f} GiB), oracle adaptive worker (arbitration loop), "
+                      f"WorkerGroupConfig(32, {cores})"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from oracle import oracle as O
+
+    cores = host_cores()
+    # each step: one 16 MiB chunk of the stream (cycling sigma and chunk index)
+    pre = []
+    for i in range(min(args.steps + args.warmup, 6)):
+        sigma = SIGMAS[i % 3]
+        pre.append(O.pack(O.generate("normal", CHUNK, (BASE_SEED + int(sigma)) ^ (i // 3), mean=MEAN, sigma=sigma)))
+    prior = [0] * 256
+    times = []
+    for s in range(args.warmup + args.steps):
+        words = pre[s % len(pre)]
+        off, cnt = O.binning_pattern(prior, 960, 8)
+        t0 = time.perf_counter()
+        hist, _, _ = O.adaptive_histogram(words, off, cnt, 960, 32, cores)
+        dt = time.perf_counter() - t0
+        prior = hist.tolist()
+        if s >= args.warmup:
+            times.append(dt)
+    total = sum(times)
+    value = CHUNK * len(times) / total / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(total / len(times) * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "step": "one 16 MiB chunk", "pattern": "CPU, from the previous step",
+                   "group_config": f"WorkerGroupConfig(32, {cores})"},
+        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": cores, "kind": "port",
+                         "sample": f"{args.steps} x 16 MiB chunks, oracle adaptive worker (arbitration loop)"},
+        "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------- device arm
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args(argv)
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    rank, world, local = dist_setup(args)
+    import torch
+
+    import paper_1011_0235_b200 as hs
+    from paper_1011_0235_b200 import _native as N
+    from paper_1011_0235_b200 import device as D
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.current_stream()
+    L = N.lib()
+
+    # ---- inputs: this rank's 3 GiB of the stream, generated in HBM (bit-exact generator)
+    streams = []
+    for j, sigma in enumerate(SIGMAS):
+        buf = torch.empty(GiB, dtype=torch.uint8, device=dev)
+        for c in range(64):
+            chunk_index = rank * 64 + c  # weak scaling: rank r owns chunks [64r, 64r+64) of each stream
+            spec = hs.SourceSpec("normal", CHUNK, (BASE_SEED + int(sigma)) ^ chunk_index, mean=MEAN, sigma=sigma)
+            hs.generate_device(spec, buf[c * CHUNK:(c + 1) * CHUNK])
+        streams.append(buf)
+    torch.cuda.synchronize()
+    begin = np.arange(64, dtype=np.uint64) * CHUNK
+    end = begin + CHUNK
+    outs = [torch.empty((64, 256), dtype=torch.int64, device=dev) for _ in SIGMAS]
+    host = [[torch.empty((64, 256), dtype=torch.int64, pin_memory=True) for _ in range(2)] for _ in SIGMAS]
+    patterns = [hs.uniform_pattern(960) for _ in SIGMAS]
+    pending: dict[int, tuple] = {}
+    flip = [0, 0, 0]
+    total_counts = torch.zeros(256, dtype=torch.int64, device=dev)
+    launch_events: list[tuple] = []
+
+    def launch(j, record=False):
+        # lag-1 pattern for stream j: its previous step's per-chunk histograms, read back
+        # asynchronously while the other streams' kernels ran
+        if j in pending:
+            ev, hb = pending.pop(j)
+            ev.synchronize()
+            prior = hb.numpy().view(np.uint64).sum(axis=0, dtype=np.uint64)
+            patterns[j] = hs.compute_binning_pattern(hs.Histogram256(prior))
+        p = patterns[j]
+        if record:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+        st = L.hs_histogram_batched(streams[j].data_ptr(), N.u64p(begin), N.u64p(end), 64, N.HS_KIND_ADAPTIVE,
+                                    N.HS_IMPL_AUTO, N.i64p(p.offset), N.i64p(p.count), 960, 8,
+                                    outs[j].data_ptr(), None, 0, stream.cuda_stream)
+        N.check(st, "hs_histogram_batched")
+        if record:
+            e1 = torch.cuda.Event(enable_timing=True)
+            e1.record(stream)
+            launch_events.append((e0, e1))
+        hb = host[j][flip[j]]
+        flip[j] ^= 1
+        hb.copy_(outs[j], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        pending[j] = (ev, hb)
+
+    def step(record=False):
+        for j in range(len(SIGMAS)):
+            launch(j, record)
+        if world > 1:
+            torch.sum(torch.stack([o.sum(dim=0) for o in outs]), dim=0, out=total_counts)
+            torch.distributed.all_reduce(total_counts)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier(world)
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        t0.record(stream)
+        for _ in range(args.steps):
+            step(record=True)
+        t1.record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    elapsed_ms = max_over_ranks(t0.elapsed_time(t1), world)
+    bytes_per_step_rank = len(SIGMAS) * GiB
+    value = world * bytes_per_step_rank * args.steps / (elapsed_ms / 1e3) / 1e9
+    launch_ms = [a.elapsed_time(b) for a, b in launch_events]
+    avg_launch_ms = float(np.mean(launch_ms))
+
+    # ---- correctness spot check of the last step against closed-form totals
+    for j in range(len(SIGMAS)):
+        got = outs[j].sum().item()
+        assert got == GiB, f"stream {j}: counted {got} != {GiB}"
+
+    # ---- roofline of the dominant kernel (k_lane<HOT>, one launch = 1 GiB, 64 segments)
+    peak, peak_src = peaks()
+    achieved = GiB / (avg_launch_ms / 1e3) / 1e9
+    traffic = None
+    tf = ROOT / "profiles" / "traffic.json"
+    if tf.exists():
+        try:
+            traffic = json.loads(tf.read_text()).get("k_lane_adaptive_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
+                "kernel": "k_lane<ADAPTIVE> (hs_histogram_batched, 64 x 16 MiB segments)",
+                "algorithmic_bytes_per_launch": GiB}
+
+    # ---- e2e through the public streaming API with pinned host buffers (rank 0 sizes it)
+    e2e = None
+    if not args.no_e2e:
+        e2e = e2e_run(hs, D, torch, streams, world, args.e2e_steps)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(streams, args.cpu_seconds)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(elapsed_ms / args.steps, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "bytes_per_step_per_gpu": bytes_per_step_rank, "chunk_bytes": CHUNK,
+                       "sigmas": list(SIGMAS), "mean": MEAN, "kernel": "adaptive", "pattern": "CPU, lag-1 per stream",
+                       "parallelism": f"shard{world}", "l2": "inputs 3 GiB/GPU >> 126 MB L2 (no flush needed)"},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": len(SIGMAS) * args.steps,
+            "clocks": clocks.summary(),
+            "per_launch_ms": {"mean": round(avg_launch_ms, 4), "min": round(min(launch_ms), 4),
+                              "max": round(max(launch_ms), 4)},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def e2e_run(hs, D, torch, streams, world, steps):
+    """The same 3-stream workload through hs.run_pipeline with every chunk in pinned
+    host memory: per iteration the producer H2D-copies a batch of 4 chunks on the copy
+    stream while the consumer's launch for the previous batch runs."""
+    chunks = []
+    for buf in streams:
+        pinned = D.pinned_bytes(GiB)
+        pinned[:] = buf.cpu().numpy()  # setup: one D2H of the generated stream (untimed)
+        words = pinned.view(np.uint32)
+        chunks.extend(hs.PackedChunk(words[c * (CHUNK // 4):(c + 1) * (CHUNK // 4)]) for c in range(64))
+    batch = 4
+    iters = len(chunks) // batch
+    cfg = hs.PipelineConfig(num_iterations=iters, chunk_pixels=CHUNK, batch_size=batch, window_size=64)
+    policy = hs.SwitchPolicy(1e-9)  # AHist for every batch, pattern from the window (lag 1)
+
+    def src():
+        for i in range(iters):
+            yield chunks[i * batch:(i + 1) * batch]
+
+    hs.run_pipeline(src(), cfg, policy)  # warm-up pass
+    torch.cuda.synchronize()
+    barrier(world)
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        acc, _, rep, log = hs.run_pipeline(src(), cfg, policy)
+        times.append(time.perf_counter() - t0)
+        assert acc.running.total() == len(chunks) * CHUNK
+    dt = max_over_ranks(float(np.median(times)), world)
+    # copy-only link bandwidth of the same pinned buffer, for the fraction
+    dst = torch.empty(GiB, dtype=torch.uint8, device="cuda")
+    h2d = []
+    big = torch.from_numpy(D.pinned_bytes(GiB))
+    for _ in range(3):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        dst.copy_(big, non_blocking=True)
+        b.record()
+        b.synchronize()
+        h2d.append(GiB / (a.elapsed_time(b) / 1e3) / 1e9)
+    total_bytes = len(chunks) * CHUNK
+    value = world * total_bytes / dt / 1e9
+    link = max(h2d)
+    return {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": total_bytes,
+            "d2h_bytes_per_step": len(chunks) * 2048, "api": "paper_1011_0235_b200.run_pipeline (pinned host chunks)",
+            "h2d_link_gbs": round(link, 2), "frac_of_link": round(value / world / link, 4)}
+
+
+if __name__ == "__main__":
+    raise SystemExit(main())
