@@ -370,7 +370,7 @@ def main(argv=None):
 
 def e2e_run(hs, D, torch, streams, world, steps):
     """The same 3-stream workload through hs.run_pipeline with every chunk in pinned
-    host memory: per iteration the producer H2D-copies a batch of 4 chunks on the copy
+    host memory: per iteration the producer H2D-copies a batch of 8 chunks on the copy
     stream while the consumer's launch for the previous batch runs."""
     chunks = []
     for buf in streams:
@@ -378,7 +378,7 @@ def e2e_run(hs, D, torch, streams, world, steps):
         pinned[:] = buf.cpu().numpy()  # setup: one D2H of the generated stream (untimed)
         words = pinned.view(np.uint32)
         chunks.extend(hs.PackedChunk(words[c * (CHUNK // 4):(c + 1) * (CHUNK // 4)]) for c in range(64))
-    batch = 4
+    batch = 8
     iters = len(chunks) // batch
     cfg = hs.PipelineConfig(num_iterations=iters, chunk_pixels=CHUNK, batch_size=batch, window_size=64)
     policy = hs.SwitchPolicy(1e-9)  # AHist for every batch, pattern from the window (lag 1)

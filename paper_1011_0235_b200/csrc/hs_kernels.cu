@@ -89,6 +89,14 @@ __device__ __forceinline__ void sh_st4(uint32_t addr, uint4 v) {
 
 __device__ __forceinline__ void compiler_fence() { asm volatile("" ::: "memory"); }
 
+// PTX prmt in its generic mode: a selector nibble with bit 3 set replicates the sign
+// (msb) of the selected byte over the output byte (__byte_perm masks that bit off)
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+  return d;
+}
+
 // byte k of w, zero-extended (PRMT)
 __device__ __forceinline__ uint32_t byte_of(uint32_t w, int k) { return __byte_perm(w, 0u, 0x4440u | k); }
 
@@ -128,9 +136,9 @@ __device__ __forceinline__ void for_each_piece(const SegParams& sp, Body&& body)
 // Streams the device byte range [p0, p1) (word aligned) through count_word(uint32)
 // and count_vec(uint4): unaligned head/tail words, then 16-B vectors in register
 // double-buffered batches of U vectors per thread.
-template <int U, int PF, class WordFn, class VecFn>
+template <int U, int PF, class WordFn, class VecFn, class BatchFn>
 __device__ __forceinline__ void stream_range(const uint8_t* __restrict__ data, uint64_t p0, uint64_t p1,
-                                             WordFn&& count_word, VecFn&& count_vec) {
+                                             WordFn&& count_word, VecFn&& count_vec, BatchFn&& count_batch) {
   const uint32_t T = blockDim.x, tid = threadIdx.x;
   // 16-B alignment is decided on absolute addresses (data itself is only word aligned)
   const uint64_t base = reinterpret_cast<uintptr_t>(data);
@@ -171,32 +179,43 @@ __device__ __forceinline__ void stream_range(const uint8_t* __restrict__ data, u
 #pragma unroll
       for (int u = 0; u < U; ++u) B[u] = ldg_stream(q + u * T);
     }
-#pragma unroll
-    for (int u = 0; u < U; ++u) count_vec(A[u]);
+    count_batch(A);
     if (j + 1 >= nfull) break;
     if (j + 2 < nfull) {
       const uint4* q = vp + (j + 2) * batch + tid;
 #pragma unroll
       for (int u = 0; u < U; ++u) A[u] = ldg_stream(q + u * T);
     }
-#pragma unroll
-    for (int u = 0; u < U; ++u) count_vec(B[u]);
+    count_batch(B);
   }
   for (uint64_t i = nfull * batch + tid; i < nv; i += T) count_vec(ldg_stream(vp + i));
 }
 
+// count_batch adapter for kernels without a batch-level decision
+template <int U, class VecFn>
+struct EachVec {
+  VecFn& f;
+  __device__ __forceinline__ void operator()(const uint4 (&v)[U]) const {
+#pragma unroll
+    for (int u = 0; u < U; ++u) f(v[u]);
+  }
+};
+template <int U, class VecFn>
+__device__ __forceinline__ EachVec<U, VecFn> each_vec(VecFn& f) { return EachVec<U, VecFn>{f}; }
+
 // ================================================================== HS_IMPL_LANE
 // Lane-private 16-bit "pair" counters. Word (lane, j) of a warp's 16 KB region counts
-// bins 2j and 2j+1 of that lane; it sits at row j (128 B) and column lane, so every
-// lane of a warp-wide atomic hits its own bank. A byte b adds 1 + (b << 16) to word
-// j = b >> 1 (one PRMT builds the increment):
-//     lo = c[2j] + c[2j+1]                  (exact while < 2^16)
-//     hi = sum(b) mod 2^16 = 2j*lo + c[2j+1] (mod 2^16)
-//  => c[2j+1] = (hi - 2j*lo) mod 2^16,  c[2j] = lo - c[2j+1]
-// Half the footprint of u32 columns, so 12 warps fit in 192 KB: the measured shared
-// atomic rate per SM grows with resident warps (tools/microbench/atoms_scaling.cu).
-// A thread may add at most 65535 bytes between flushes; pieces are capped at
-// kLaneFlushBytes per CTA (<= 16 MiB / 384 threads = 43.7 K bytes per thread).
+// bins j and j+128 of that lane; it sits at row j (128 B) and column lane, so every
+// lane of a warp-wide atomic hits its own bank. A byte b adds to word j = b & 127
+//     inc = 1 + (b >= 128 ? 0xFF << 16 : 0)      (one PRMT in sign-replicate mode)
+// so  lo = c[j] + c[j+128]                 (exact while < 2^16)
+//     hi = 255 * c[j+128]  (mod 2^16)
+//  => c[j+128] = hi * 255^-1 = hi * 65279 (mod 2^16),  c[j] = lo - c[j+128]
+// (255 is odd, hence invertible mod 2^16.) Half the footprint of u32 columns, so 12
+// warps fit in 192 KB: the measured shared-atomic rate per SM grows with resident
+// warps (tools/microbench/atoms_scaling.cu). A thread may add at most 65535 bytes
+// between flushes; pieces are capped at kLaneFlushBytes per CTA
+// (<= 16 MiB / 384 threads = 43.7 K bytes per thread).
 constexpr int kLaneWarps = 12;
 constexpr int kLaneThreads = 32 * kLaneWarps;
 constexpr uint32_t kLaneRegionBytes = 128 * 32 * 4;  // 128 pair rows x 32 lanes x u32
@@ -206,8 +225,9 @@ constexpr uint64_t kLaneFlushBytes = 16ull << 20;
 // Adds the CTA's pair counters into out[256] and re-zeroes them.
 // Phase 1: lane l of warp w decodes rows l, l+32, l+64, l+96 of its own region (each
 // row read as 8 x 16-B chunks, staggered by lane so each quarter-warp is conflict
-// free) and parks the two bin sums of row r in words (2r)&31 and (2r+1)&31.
-// Phase 2: thread b sums the parked word of bin b over the warps (bank b & 31).
+// free) and parks the sums of bins r and r+128 in words r&31 and (r+16)&31 of row r.
+// Phase 2: thread b sums the parked word of bin b over the warps.
+template <int PAIR>
 __device__ __forceinline__ void lane_flush(uint32_t sbase, unsigned long long* __restrict__ out) {
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   compiler_fence();
@@ -225,12 +245,13 @@ __device__ __forceinline__ void lane_flush(uint32_t sbase, unsigned long long* _
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const uint32_t lo = x4[q] & 0xffffu, hi = x4[q] >> 16;
-        const uint32_t odd = (hi - 2 * r * lo) & 0xffffu;
-        so += odd;
-        se += lo - odd;
+        // PAIR 0: c[r + 128] = hi * 255^-1; PAIR 1: c[2r + 1] = hi - 2r * lo (mod 2^16)
+        const uint32_t high = PAIR == 0 ? (hi * 65279u) & 0xffffu : (hi - 2 * r * lo) & 0xffffu;
+        so += high;
+        se += lo - high;
       }
     }
-    const uint32_t pe = (2 * r) & 31, po = (2 * r + 1) & 31;
+    const uint32_t pe = PAIR == 0 ? r & 31 : (2 * r) & 31, po = PAIR == 0 ? (r + 16) & 31 : (2 * r + 1) & 31;
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       const uint32_t chunk = (c + lane) & 7;
@@ -249,7 +270,9 @@ __device__ __forceinline__ void lane_flush(uint32_t sbase, unsigned long long* _
     unsigned long long tot = 0;
 #pragma unroll
     for (int w = 0; w < kLaneWarps; ++w) {
-      const uint32_t a = sbase + w * kLaneRegionBytes + (b >> 1) * 128 + ((b & 31) << 2);
+      const uint32_t r = PAIR == 0 ? b & 127 : b >> 1;
+      const uint32_t word_ix = PAIR == 0 ? (b < 128 ? (r & 31) : ((r + 16) & 31)) : (b & 31);
+      const uint32_t a = sbase + w * kLaneRegionBytes + r * 128 + (word_ix << 2);
       tot += sh_ld(a);
       sh_st(a, 0);
     }
@@ -259,7 +282,7 @@ __device__ __forceinline__ void lane_flush(uint32_t sbase, unsigned long long* _
   __syncthreads();
 }
 
-template <int U, int PF, bool HOT>
+template <int U, int PF, bool HOT, int PAIR = 0>
 __global__ void __launch_bounds__(kLaneThreads, 1)
     k_lane(const uint8_t* __restrict__ data, const __grid_constant__ SegParams sp, int hot_bin,
            unsigned long long* __restrict__ out) {
@@ -277,27 +300,42 @@ __global__ void __launch_bounds__(kLaneThreads, 1)
   uint32_t hotcnt = 0;
 
   auto word = [&](uint32_t w) {
-    const uint32_t h = (w >> 1) & 0x7f7f7f7fu;  // pair row of each byte
-    sh_add(tb + (byte_of(h, 0) << 7), __byte_perm(w, 1u, 0x7054u));
-    sh_add(tb + (byte_of(h, 1) << 7), __byte_perm(w, 1u, 0x7154u));
-    sh_add(tb + (byte_of(h, 2) << 7), __byte_perm(w, 1u, 0x7254u));
-    sh_add(tb + (byte_of(h, 3) << 7), __byte_perm(w, 1u, 0x7354u));
+    if (PAIR == 0) {
+      const uint32_t m = w & 0x7f7f7f7fu;  // pair row (b & 127) of each byte
+      sh_add(tb + (byte_of(m, 0) << 7), prmt(w, 1u, 0x7854u));
+      sh_add(tb + (byte_of(m, 1) << 7), prmt(w, 1u, 0x7954u));
+      sh_add(tb + (byte_of(m, 2) << 7), prmt(w, 1u, 0x7a54u));
+      sh_add(tb + (byte_of(m, 3) << 7), prmt(w, 1u, 0x7b54u));
+    } else {
+      const uint32_t h = (w >> 1) & 0x7f7f7f7fu;  // pair row (b >> 1) of each byte
+      sh_add(tb + (byte_of(h, 0) << 7), __byte_perm(w, 1u, 0x7054u));
+      sh_add(tb + (byte_of(h, 1) << 7), __byte_perm(w, 1u, 0x7154u));
+      sh_add(tb + (byte_of(h, 2) << 7), __byte_perm(w, 1u, 0x7254u));
+      sh_add(tb + (byte_of(h, 3) << 7), __byte_perm(w, 1u, 0x7354u));
+    }
   };
+  auto plain = [&](const uint4& v) { word(v.x); word(v.y); word(v.z); word(v.w); };
   auto vec = [&](const uint4& v) {
     if (HOT) {
       const uint32_t d = (v.x ^ hot4) | (v.y ^ hot4) | (v.z ^ hot4) | (v.w ^ hot4);
       if (d == 0) { hotcnt += 16; return; }
     }
-    word(v.x); word(v.y); word(v.z); word(v.w);
+    plain(v);
   };
+  // ADAPTIVE tests every 16-B vector against the CPU pattern's hot bin. (A warp-uniform
+  // test per batch issues fewer instructions but measured 11% slower on normal data:
+  // the duplicated batch bodies overflow the instruction cache.)
   for_each_piece<kLaneFlushBytes>(sp, [&](int s, uint64_t p0, uint64_t p1) {
-    stream_range<U, PF>(data, p0, p1, word, vec);
+    stream_range<U, PF>(data, p0, p1, word, vec, each_vec<U>(vec));
     if (HOT) {
-      // hotcnt hits of byte `hot`: lo += hotcnt, hi += hotcnt * hot (mod 2^16)
-      if (hotcnt) sh_add(tb + ((hot >> 1) << 7), hotcnt * (1u + (hot << 16)));
+      // hotcnt hits of byte `hot` (PAIR 0: hi += 255 per high-bin hit; PAIR 1: hi += hot per hit)
+      if (hotcnt) {
+        if (PAIR == 0) sh_add(tb + ((hot & 127) << 7), hotcnt * (hot >= 128 ? 0x00ff0001u : 1u));
+        else sh_add(tb + ((hot >> 1) << 7), hotcnt * (1u + (hot << 16)));
+      }
       hotcnt = 0;
     }
-    lane_flush(sbase, out + size_t(sp.out_base + s) * 256);
+    lane_flush<PAIR>(sbase, out + size_t(sp.out_base + s) * 256);
   });
 }
 
@@ -321,7 +359,7 @@ __global__ void __launch_bounds__(kWarpThreads)
   };
   auto vec = [&](const uint4& v) { word(v.x); word(v.y); word(v.z); word(v.w); };
   for_each_piece<kBigCap>(sp, [&](int s, uint64_t p0, uint64_t p1) {
-    stream_range<U, PF>(data, p0, p1, word, vec);
+    stream_range<U, PF>(data, p0, p1, word, vec, each_vec<U>(vec));
     compiler_fence();
     __syncthreads();
     const int b = threadIdx.x;
@@ -366,7 +404,7 @@ __global__ void __launch_bounds__(kSubThreads)
   };
   auto vec = [&](const uint4& v) { word(v.x); word(v.y); word(v.z); word(v.w); };
   for_each_piece<kBigCap>(sp, [&](int s, uint64_t p0, uint64_t p1) {
-    stream_range<U, PF>(data, p0, p1, word, vec);
+    stream_range<U, PF>(data, p0, p1, word, vec, each_vec<U>(vec));
     compiler_fence();
     __syncthreads();
     // reduce_subbins fused: bin b = sum of its count[b] slots over the 8 warps
@@ -447,7 +485,7 @@ __global__ void __launch_bounds__(kSubThreads)
   auto vec = [&](const uint4& v) { word(v.x); word(v.y); word(v.z); word(v.w); };
   uint64_t vb, ve;
   block_range(n_bytes, vb, ve);
-  if (vb < ve) stream_range<8, 2>(data, vb, ve, word, vec);
+  if (vb < ve) stream_range<8, 2>(data, vb, ve, word, vec, each_vec<8>(vec));
   compiler_fence();
   __syncthreads();
   if (stage <= HS_STAGE_PATTERN_LOAD) {
@@ -575,20 +613,13 @@ int set_smem(K kernel, size_t bytes) {
   return fold(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
 }
 
-// development knobs for tuning runs (tools/kbench.py); production uses the defaults
-int lane_u() {
-  static int u = [] {
-    const char* s = getenv("HS_LANE_U");
-    return s ? atoi(s) : 8;
-  }();
-  return u;
-}
-int lane_pf() {
-  static int p = [] {
-    const char* s = getenv("HS_LANE_PF");
+// development knob for A/B tuning runs (tools/kbench.py); production uses variant 0
+int lane_variant() {
+  static int v = [] {
+    const char* s = getenv("HS_LANE_VARIANT");
     return s ? atoi(s) : 0;
   }();
-  return p;
+  return v;
 }
 
 // one launch over <= kMaxSeg segments
@@ -615,21 +646,19 @@ int launch_batch(const uint8_t* d_data, const uint64_t* h_begin, const uint64_t*
     const bool hot = kind == HS_KIND_ADAPTIVE;
     const int hb = pp ? pp->hot_bin : 0;
     int rc;
-#define HS_LAUNCH_LANE(UU, PP)                                                                 \
-  if (hot) {                                                                                   \
-    if ((rc = set_smem(k_lane<UU, PP, true>, kLaneSmem)) != HS_OK) return rc;                  \
-    k_lane<UU, PP, true><<<grid, kLaneThreads, kLaneSmem, st>>>(d_data, sp, hb, d_out);        \
-  } else {                                                                                     \
-    if ((rc = set_smem(k_lane<UU, PP, false>, kLaneSmem)) != HS_OK) return rc;                 \
-    k_lane<UU, PP, false><<<grid, kLaneThreads, kLaneSmem, st>>>(d_data, sp, hb, d_out);       \
+#define HS_LAUNCH_LANE(UU, PP, PA)                                                                   \
+  if (hot) {                                                                                         \
+    if ((rc = set_smem(k_lane<UU, PP, true, PA>, kLaneSmem)) != HS_OK) return rc;                    \
+    k_lane<UU, PP, true, PA><<<grid, kLaneThreads, kLaneSmem, st>>>(d_data, sp, hb, d_out);          \
+  } else {                                                                                           \
+    if ((rc = set_smem(k_lane<UU, PP, false, PA>, kLaneSmem)) != HS_OK) return rc;                   \
+    k_lane<UU, PP, false, PA><<<grid, kLaneThreads, kLaneSmem, st>>>(d_data, sp, hb, d_out);         \
   }
-    switch (lane_u() * 16 + lane_pf()) {
-      case 8 * 16 + 1: HS_LAUNCH_LANE(8, 1) break;
-      case 8 * 16 + 2: HS_LAUNCH_LANE(8, 2) break;
-      case 6 * 16 + 0: HS_LAUNCH_LANE(6, 0) break;
-      case 4 * 16 + 0: HS_LAUNCH_LANE(4, 0) break;
-      case 4 * 16 + 2: HS_LAUNCH_LANE(4, 2) break;
-      default: HS_LAUNCH_LANE(8, 0) break;
+    switch (lane_variant()) {
+      case 1: HS_LAUNCH_LANE(8, 0, 1) break;   // byte-sum pairing (2j, 2j+1)
+      case 2: HS_LAUNCH_LANE(4, 0, 0) break;
+      case 3: HS_LAUNCH_LANE(8, 1, 0) break;   // + bulk L2 prefetch one batch ahead
+      default: HS_LAUNCH_LANE(8, 0, 0) break;  // production
     }
 #undef HS_LAUNCH_LANE
   } else if (impl == HS_IMPL_WARP) {

@@ -1,8 +1,7 @@
 #!/bin/bash
-# tuning sweep of the lane-private kernel's batch size (U) and L2 prefetch distance (PF)
-for cfg in "8 0" "8 1" "8 2" "6 0" "4 0" "4 2"; do
-  set -- $cfg
-  for d in "uniform naive" "normal32 adaptive" "const127 adaptive"; do
-    echo -n "U=$1 PF=$2 "; HS_LANE_U=$1 HS_LANE_PF=$2 python tools/kbench.py $d lane $((1<<30)) 8
+# A/B of lane-kernel variants (HS_LANE_VARIANT, see launch_batch in hs_kernels.cu)
+for v in ${VARIANTS:-0 1 2 3}; do
+  for d in "uniform naive" "normal8 adaptive" "normal32 adaptive" "normal64 adaptive" "const127 adaptive"; do
+    echo -n "v=$v "; HS_LANE_VARIANT=$v python tools/kbench.py $d lane $((1<<30)) 10
   done
 done
