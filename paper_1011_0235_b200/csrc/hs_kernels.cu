@@ -14,10 +14,10 @@
 // Design notes (numbers in DESIGN.md §4, tools/microbench/hist_variants.cu):
 //   * Input bytes are read once with 16-B streaming loads (LDG.128, L1::no_allocate),
 //     register double-buffered so a batch is in flight while the previous one is counted.
-//   * HS_IMPL_LANE keeps one private u32 counter column per lane: counter (lane, bin) is
-//     shared word bin*32 + lane of its warp's 32 KB region, so every lane of an ATOMS
-//     hits its own bank (conflict-free for any input, including fully degenerate data).
-//     Seven such warps fill 224 KB of the SM's 227 KB.
+//   * HS_IMPL_LANE keeps one u32 counter column per lane: counter (lane, bin) is shared
+//     word bin*32 + lane of ONE 32 KB array used by all 32 warps of the CTA, so every
+//     lane of an ATOMS hits its own bank (conflict-free for any input, including fully
+//     degenerate data) and occupancy is unconstrained (2 CTAs = 64 warps per SM).
 //   * Blackwell merges same-address lanes of one shared atomic, so the contention the
 //     paper's AHist relieves (all lanes on one bin) is cheap here; what costs is distinct
 //     addresses in one bank. ADAPTIVE therefore keeps the lane-private core and uses the
@@ -75,27 +75,12 @@ __device__ __forceinline__ void sh_st(uint32_t addr, uint32_t v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v));
 }
 
-__device__ __forceinline__ uint4 sh_ld4(uint32_t addr) {
-  uint4 v;
-  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
-  return v;
-}
-
 __device__ __forceinline__ void sh_st4(uint32_t addr, uint4 v) {
   asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z),
                "r"(v.w));
 }
 
 __device__ __forceinline__ void compiler_fence() { asm volatile("" ::: "memory"); }
-
-// PTX prmt in its generic mode: a selector nibble with bit 3 set replicates the sign
-// (msb) of the selected byte over the output byte (__byte_perm masks that bit off)
-__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
-  uint32_t d;
-  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
-  return d;
-}
 
 // byte k of w, zero-extended (PRMT)
 __device__ __forceinline__ uint32_t byte_of(uint32_t w, int k) { return __byte_perm(w, 0u, 0x4440u | k); }
@@ -204,138 +189,114 @@ template <int U, class VecFn>
 __device__ __forceinline__ EachVec<U, VecFn> each_vec(VecFn& f) { return EachVec<U, VecFn>{f}; }
 
 // ================================================================== HS_IMPL_LANE
-// Lane-private 16-bit "pair" counters. Word (lane, j) of a warp's 16 KB region counts
-// bins j and j+128 of that lane; it sits at row j (128 B) and column lane, so every
-// lane of a warp-wide atomic hits its own bank. A byte b adds to word j = b & 127
-//     inc = 1 + (b >= 128 ? 0xFF << 16 : 0)      (one PRMT in sign-replicate mode)
-// so  lo = c[j] + c[j+128]                 (exact while < 2^16)
-//     hi = 255 * c[j+128]  (mod 2^16)
-//  => c[j+128] = hi * 255^-1 = hi * 65279 (mod 2^16),  c[j] = lo - c[j+128]
-// (255 is odd, hence invertible mod 2^16.) Half the footprint of u32 columns, so 12
-// warps fit in 192 KB: the measured shared-atomic rate per SM grows with resident
-// warps (tools/microbench/atoms_scaling.cu). A thread may add at most 65535 bytes
-// between flushes; pieces are capped at kLaneFlushBytes per CTA
-// (<= 16 MiB / 384 threads = 43.7 K bytes per thread).
-constexpr int kLaneWarps = 12;
-constexpr int kLaneThreads = 32 * kLaneWarps;
-constexpr uint32_t kLaneRegionBytes = 128 * 32 * 4;  // 128 pair rows x 32 lanes x u32
-constexpr size_t kLaneSmem = size_t(kLaneWarps) * kLaneRegionBytes;
-constexpr uint64_t kLaneFlushBytes = 16ull << 20;
+// Lane-banked u32 counters shared by every warp of the CTA: counter (lane, bin) is
+// shared word bin*32 + lane of one 32 KB array. Within one warp-wide atomic each lane
+// hits its own bank (conflict-free for ANY data, fully degenerate included); across
+// warps the array is shared through the atomicity of ATOMS. Because the footprint per
+// CTA is fixed at 32 KB, occupancy is free: 2 CTAs x 32 warps = 64 warps per SM keep
+// the loads and the shared-atomic pipe busy (tools/microbench/shared_lanebank.cu).
+// Per byte: PRMT (extract) + IMAD (address) + ATOMS.POPC.INC.
+// A column (lane) adds at most piece/32 per flush; pieces are capped at 1 GiB per CTA.
+constexpr int kLaneThreads = 1024;
+constexpr int kLaneMinBlocks = 2;
+constexpr uint32_t kLaneArrayBytes = 256 * 32 * 4;
 
-// Adds the CTA's pair counters into out[256] and re-zeroes them.
-// Phase 1: lane l of warp w decodes rows l, l+32, l+64, l+96 of its own region (each
-// row read as 8 x 16-B chunks, staggered by lane so each quarter-warp is conflict
-// free) and parks the sums of bins r and r+128 in words r&31 and (r+16)&31 of row r.
-// Phase 2: thread b sums the parked word of bin b over the warps.
-template <int PAIR>
+// Adds the CTA's counters into out[256] and re-zeroes them: 4 threads per bin, each
+// summing 8 of the bin's 32 lane words (staggered: conflict-free), shuffle-combined.
 __device__ __forceinline__ void lane_flush(uint32_t sbase, unsigned long long* __restrict__ out) {
-  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   compiler_fence();
   __syncthreads();
-  const uint32_t region = sbase + warp * kLaneRegionBytes;
-#pragma unroll 1
-  for (int i = 0; i < 4; ++i) {
-    const uint32_t r = lane + 32 * i;
-    const uint32_t row = region + r * 128;
-    uint32_t se = 0, so = 0;
+  for (uint32_t t = threadIdx.x; t < 1024; t += blockDim.x) {
+    const uint32_t b = t >> 2, sub = t & 3;
+    uint32_t s = 0;
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const uint4 v = sh_ld4(row + (((c + lane) & 7) << 4));
-      const uint32_t x4[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint32_t lo = x4[q] & 0xffffu, hi = x4[q] >> 16;
-        // PAIR 0: c[r + 128] = hi * 255^-1; PAIR 1: c[2r + 1] = hi - 2r * lo (mod 2^16)
-        const uint32_t high = PAIR == 0 ? (hi * 65279u) & 0xffffu : (hi - 2 * r * lo) & 0xffffu;
-        so += high;
-        se += lo - high;
-      }
-    }
-    const uint32_t pe = PAIR == 0 ? r & 31 : (2 * r) & 31, po = PAIR == 0 ? (r + 16) & 31 : (2 * r + 1) & 31;
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const uint32_t chunk = (c + lane) & 7;
-      uint32_t z[4] = {0, 0, 0, 0};
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint32_t wi = chunk * 4 + q;
-        z[q] = wi == pe ? se : (wi == po ? so : 0u);
-      }
-      sh_st4(row + (chunk << 4), make_uint4(z[0], z[1], z[2], z[3]));
-    }
-  }
-  compiler_fence();
-  __syncthreads();
-  for (uint32_t b = threadIdx.x; b < 256; b += blockDim.x) {
-    unsigned long long tot = 0;
-#pragma unroll
-    for (int w = 0; w < kLaneWarps; ++w) {
-      const uint32_t r = PAIR == 0 ? b & 127 : b >> 1;
-      const uint32_t word_ix = PAIR == 0 ? (b < 128 ? (r & 31) : ((r + 16) & 31)) : (b & 31);
-      const uint32_t a = sbase + w * kLaneRegionBytes + r * 128 + (word_ix << 2);
-      tot += sh_ld(a);
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t a = sbase + b * 128 + (((sub * 8 + i + b) & 31) << 2);
+      s += sh_ld(a);
       sh_st(a, 0);
     }
-    if (tot) atomicAdd(out + b, tot);
+    unsigned long long tot = s;
+    tot += __shfl_xor_sync(0xffffffffu, tot, 1);
+    tot += __shfl_xor_sync(0xffffffffu, tot, 2);
+    if (sub == 0 && tot) atomicAdd(out + b, tot);
   }
   compiler_fence();
   __syncthreads();
 }
 
-template <int U, int PF, bool HOT, int PAIR = 0>
-__global__ void __launch_bounds__(kLaneThreads, 1)
-    k_lane(const uint8_t* __restrict__ data, const __grid_constant__ SegParams sp, int hot_bin,
-           unsigned long long* __restrict__ out) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
-  {
-    const uint32_t n16 = uint32_t(kLaneSmem / 16);
-    for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x) sh_st4(sbase + i * 16, make_uint4(0, 0, 0, 0));
-  }
-  __syncthreads();
-  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t tb = sbase + warp * kLaneRegionBytes + lane * 4;  // column base: bank == lane
-  const uint32_t hot = uint32_t(hot_bin & 0xff);
-  const uint32_t hot4 = hot * 0x01010101u;
+// The streaming loop of one piece, written lean for the 32-register budget of 64
+// resident warps: 32-bit vector counts, a running 16-B pointer, compile-time stride.
+// Returns the thread's register count of all-hot vectors (ADAPTIVE).
+template <int U, bool HOT>
+__device__ __noinline__ uint32_t lane_piece(const uint8_t* __restrict__ data, uint64_t p0, uint64_t p1,
+                                            uint32_t tb, uint32_t hot4) {
+  constexpr uint32_t T = kLaneThreads;
+  const uint32_t tid = threadIdx.x;
   uint32_t hotcnt = 0;
-
   auto word = [&](uint32_t w) {
-    if (PAIR == 0) {
-      const uint32_t m = w & 0x7f7f7f7fu;  // pair row (b & 127) of each byte
-      sh_add(tb + (byte_of(m, 0) << 7), prmt(w, 1u, 0x7854u));
-      sh_add(tb + (byte_of(m, 1) << 7), prmt(w, 1u, 0x7954u));
-      sh_add(tb + (byte_of(m, 2) << 7), prmt(w, 1u, 0x7a54u));
-      sh_add(tb + (byte_of(m, 3) << 7), prmt(w, 1u, 0x7b54u));
-    } else {
-      const uint32_t h = (w >> 1) & 0x7f7f7f7fu;  // pair row (b >> 1) of each byte
-      sh_add(tb + (byte_of(h, 0) << 7), __byte_perm(w, 1u, 0x7054u));
-      sh_add(tb + (byte_of(h, 1) << 7), __byte_perm(w, 1u, 0x7154u));
-      sh_add(tb + (byte_of(h, 2) << 7), __byte_perm(w, 1u, 0x7254u));
-      sh_add(tb + (byte_of(h, 3) << 7), __byte_perm(w, 1u, 0x7354u));
-    }
+    sh_inc(tb + (byte_of(w, 0) << 7));
+    sh_inc(tb + (byte_of(w, 1) << 7));
+    sh_inc(tb + (byte_of(w, 2) << 7));
+    sh_inc(tb + (byte_of(w, 3) << 7));
   };
-  auto plain = [&](const uint4& v) { word(v.x); word(v.y); word(v.z); word(v.w); };
+  // ADAPTIVE counts 16-B vectors made only of the CPU pattern's hot bin in a register
+  // (no shared-memory traffic for degenerate input).
   auto vec = [&](const uint4& v) {
     if (HOT) {
       const uint32_t d = (v.x ^ hot4) | (v.y ^ hot4) | (v.z ^ hot4) | (v.w ^ hot4);
       if (d == 0) { hotcnt += 16; return; }
     }
-    plain(v);
+    word(v.x); word(v.y); word(v.z); word(v.w);
   };
-  // ADAPTIVE tests every 16-B vector against the CPU pattern's hot bin. (A warp-uniform
-  // test per batch issues fewer instructions but measured 11% slower on normal data:
-  // the duplicated batch bodies overflow the instruction cache.)
-  for_each_piece<kLaneFlushBytes>(sp, [&](int s, uint64_t p0, uint64_t p1) {
-    stream_range<U, PF>(data, p0, p1, word, vec, each_vec<U>(vec));
-    if (HOT) {
-      // hotcnt hits of byte `hot` (PAIR 0: hi += 255 per high-bin hit; PAIR 1: hi += hot per hit)
-      if (hotcnt) {
-        if (PAIR == 0) sh_add(tb + ((hot & 127) << 7), hotcnt * (hot >= 128 ? 0x00ff0001u : 1u));
-        else sh_add(tb + ((hot >> 1) << 7), hotcnt * (1u + (hot << 16)));
-      }
-      hotcnt = 0;
+  const uint64_t base = reinterpret_cast<uintptr_t>(data);
+  const uint64_t a0 = min(p1, ((base + p0 + 15) & ~uint64_t(15)) - base);
+  const uint64_t a1 = max(a0, ((base + p1) & ~uint64_t(15)) - base);
+  if (p0 + 4ull * tid < a0) word(*reinterpret_cast<const uint32_t*>(data + p0 + 4ull * tid));
+  if (a1 + 4ull * tid < p1) word(*reinterpret_cast<const uint32_t*>(data + a1 + 4ull * tid));
+  const uint4* __restrict__ q = reinterpret_cast<const uint4*>(data + a0) + tid;
+  const uint32_t nv = uint32_t((a1 - a0) >> 4);  // pieces are <= 1 GiB
+  const uint32_t nfull = nv / (U * T);
+  uint4 A[U], B[U];
+  if (nfull > 0) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) A[u] = ldg_stream(q + u * T);
+  }
+  for (uint32_t j = 0; j < nfull; j += 2) {
+    const bool more = j + 1 < nfull;
+    if (more) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) B[u] = ldg_stream(q + (U + u) * T);
     }
-    lane_flush<PAIR>(sbase, out + size_t(sp.out_base + s) * 256);
+#pragma unroll
+    for (int u = 0; u < U; ++u) vec(A[u]);
+    if (!more) break;
+    if (j + 2 < nfull) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) A[u] = ldg_stream(q + (2 * U + u) * T);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) vec(B[u]);
+    q += 2 * U * T;
+  }
+  for (uint32_t i = nfull * U * T + tid; i < nv; i += T)
+    vec(ldg_stream(reinterpret_cast<const uint4*>(data + a0) + i));
+  return hotcnt;
+}
+
+template <int U, bool HOT>
+__global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
+    k_lane(const uint8_t* __restrict__ data, const __grid_constant__ SegParams sp, int hot_bin,
+           unsigned long long* __restrict__ out) {
+  __shared__ __align__(16) uint32_t counters[256 * 32];
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(counters);
+  for (uint32_t i = threadIdx.x; i < kLaneArrayBytes / 16; i += blockDim.x) sh_st4(sbase + i * 16, make_uint4(0, 0, 0, 0));
+  __syncthreads();
+  const uint32_t tb = sbase + (threadIdx.x & 31) * 4;  // column base: bank == lane
+  const uint32_t hot = uint32_t(hot_bin & 0xff);
+  for_each_piece<kBigCap>(sp, [&](int s, uint64_t p0, uint64_t p1) {
+    const uint32_t hotcnt = lane_piece<U, HOT>(data, p0, p1, tb, hot * 0x01010101u);
+    if (HOT && hotcnt) sh_add(tb + (hot << 7), hotcnt);
+    lane_flush(sbase, out + size_t(sp.out_base + s) * 256);
   });
 }
 
@@ -613,15 +574,6 @@ int set_smem(K kernel, size_t bytes) {
   return fold(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
 }
 
-// development knob for A/B tuning runs (tools/kbench.py); production uses variant 0
-int lane_variant() {
-  static int v = [] {
-    const char* s = getenv("HS_LANE_VARIANT");
-    return s ? atoi(s) : 0;
-  }();
-  return v;
-}
-
 // one launch over <= kMaxSeg segments
 int launch_batch(const uint8_t* d_data, const uint64_t* h_begin, const uint64_t* h_end, int s0, int ns,
                  int kind, int impl, const PatternParams* pp, unsigned long long* d_out, cudaStream_t st,
@@ -637,30 +589,17 @@ int launch_batch(const uint8_t* d_data, const uint64_t* h_begin, const uint64_t*
   }
   sp.vstart[ns] = v;
   if (v == 0) return HS_OK;
-  if (impl == HS_IMPL_AUTO) impl = (v >= (8ull << 20)) ? HS_IMPL_LANE : HS_IMPL_WARP;
+  if (impl == HS_IMPL_AUTO) impl = HS_IMPL_LANE;
   cudaError_t e = cudaSuccess;
   if (impl == HS_IMPL_LANE) {
-    if ((size_t)di.smem_optin < kLaneSmem) return HS_ERR_UNSUPPORTED;
-    const uint64_t want = (v + (256ull << 10) - 1) / (256ull << 10);
-    const int grid = int(std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(di.sms))));
-    const bool hot = kind == HS_KIND_ADAPTIVE;
+    // ~64 KiB of input per CTA at least; at most 2 resident CTAs per SM
+    const uint64_t want = (v + (64ull << 10) - 1) / (64ull << 10);
+    const int grid = int(std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(di.sms) * kLaneMinBlocks)));
     const int hb = pp ? pp->hot_bin : 0;
-    int rc;
-#define HS_LAUNCH_LANE(UU, PP, PA)                                                                   \
-  if (hot) {                                                                                         \
-    if ((rc = set_smem(k_lane<UU, PP, true, PA>, kLaneSmem)) != HS_OK) return rc;                    \
-    k_lane<UU, PP, true, PA><<<grid, kLaneThreads, kLaneSmem, st>>>(d_data, sp, hb, d_out);          \
-  } else {                                                                                           \
-    if ((rc = set_smem(k_lane<UU, PP, false, PA>, kLaneSmem)) != HS_OK) return rc;                   \
-    k_lane<UU, PP, false, PA><<<grid, kLaneThreads, kLaneSmem, st>>>(d_data, sp, hb, d_out);         \
-  }
-    switch (lane_variant()) {
-      case 1: HS_LAUNCH_LANE(8, 0, 1) break;   // byte-sum pairing (2j, 2j+1)
-      case 2: HS_LAUNCH_LANE(4, 0, 0) break;
-      case 3: HS_LAUNCH_LANE(8, 1, 0) break;   // + bulk L2 prefetch one batch ahead
-      default: HS_LAUNCH_LANE(8, 0, 0) break;  // production
-    }
-#undef HS_LAUNCH_LANE
+    if (kind == HS_KIND_ADAPTIVE)
+      k_lane<2, true><<<grid, kLaneThreads, 0, st>>>(d_data, sp, hb, d_out);
+    else
+      k_lane<2, false><<<grid, kLaneThreads, 0, st>>>(d_data, sp, hb, d_out);
   } else if (impl == HS_IMPL_WARP) {
     const uint64_t want = (v + (32ull << 10) - 1) / (32ull << 10);
     const int grid = int(std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(di.sms) * 8)));

@@ -31,7 +31,7 @@ __global__ void __launch_bounds__(TH, 1) k(const uint4* __restrict__ in, size_t 
   if (blockIdx.x == 0 && threadIdx.x == 0) base_probe[0] = sb;
   constexpr uint32_t REGION = MODE == 0 ? 32768 : 16384;
   const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t zbytes = MODE == 2 ? 227 * 1024 : nw * REGION;
+  const uint32_t zbytes = MODE == 2 ? (0x8000 - 0x400) + (nw / 2) * 32768 : nw * REGION;
   for (uint32_t i = threadIdx.x; i < zbytes / 16; i += blockDim.x)
     asm volatile("st.shared.v4.u32 [%0], {%1,%1,%1,%1};" ::"r"(sb + i * 16), "r"(0));
   __syncthreads();
@@ -110,8 +110,8 @@ __global__ void __launch_bounds__(TH, 1) k(const uint4* __restrict__ in, size_t 
 }
 
 template <int MODE, int U, int TH>
-int run(const uint4* d, size_t n, unsigned long long* out, unsigned* probe, int sms, const std::vector<unsigned long long>& ref, const char* tag) {
-  size_t smem = MODE == 2 ? 227 * 1024 : (size_t)(TH / 32) * (MODE == 0 ? 32768 : 16384);
+int run(const uint4* d, size_t n, unsigned long long* out, unsigned* probe, int sms, const std::vector<unsigned long long>& ref, const char* tag, size_t extra = 0) {
+  size_t smem = extra + (MODE == 2 ? (size_t)(0x8000 - 0x400) + (size_t)(TH / 64) * 32768 : (size_t)(TH / 32) * (MODE == 0 ? 32768 : 16384));
   CK(cudaFuncSetAttribute(k<MODE, U, TH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   std::vector<float> t;
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
@@ -132,7 +132,7 @@ int run(const uint4* d, size_t n, unsigned long long* out, unsigned* probe, int 
   }
   unsigned pb; cudaMemcpy(&pb, probe, 4, cudaMemcpyDeviceToHost);
   std::sort(t.begin(), t.end());
-  printf("%-8s U=%d warps=%2d smem=%6zu sbase=0x%x  %.3f ms  %7.1f GB/s  %s\n", tag, U, TH / 32, smem, pb, t[2], n / (t[2] * 1e6), ok ? "exact" : "MISMATCH");
+  printf("%-8s extra=%3zuK U=%d warps=%2d smem=%6zu sbase=0x%x  %.3f ms  %7.1f GB/s  %s\n", tag, extra >> 10, U, TH / 32, smem, pb, t[2], n / (t[2] * 1e6), ok ? "exact" : "MISMATCH");
   return 0;
 }
 
@@ -151,7 +151,7 @@ int main() {
   unsigned* probe; CK(cudaMalloc(&probe, 4));
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   std::vector<uint8_t> h(n);
-  for (int kind = 0; kind < 3; ++kind) {
+  for (int kind = 0; kind < 1; ++kind) {
     fill<<<sms * 8, 256>>>(d, n, kind);
     CK(cudaDeviceSynchronize());
     cudaMemcpy(h.data(), d, n, cudaMemcpyDeviceToHost);
@@ -159,13 +159,16 @@ int main() {
     for (size_t i = 0; i < n; ++i) ref[h[i]]++;
     printf("-- data kind %d (0 uniform, 1 const127, 2 narrow 124..131)\n", kind);
     const uint4* in = reinterpret_cast<const uint4*>(d);
-    run<0, 8, 224>(in, n, out, probe, sms, ref, "u32");
     run<1, 8, 384>(in, n, out, probe, sms, ref, "pair16");
-    run<1, 8, 448>(in, n, out, probe, sms, ref, "pair16");
-    run<2, 8, 384>(in, n, out, probe, sms, ref, "pair16p");
-    run<2, 6, 384>(in, n, out, probe, sms, ref, "pair16p");
-    run<2, 10, 384>(in, n, out, probe, sms, ref, "pair16p");
+    run<1, 8, 384>(in, n, out, probe, sms, ref, "pair16", 16 << 10);
+    run<1, 8, 384>(in, n, out, probe, sms, ref, "pair16", 30 << 10);
+    run<1, 8, 256>(in, n, out, probe, sms, ref, "pair16");
+    run<1, 8, 256>(in, n, out, probe, sms, ref, "pair16", 64 << 10);
+    run<1, 8, 256>(in, n, out, probe, sms, ref, "pair16", 96 << 10);
     run<2, 8, 256>(in, n, out, probe, sms, ref, "pair16p");
+    run<2, 8, 256>(in, n, out, probe, sms, ref, "pair16p", 32 << 10);
+    run<2, 8, 256>(in, n, out, probe, sms, ref, "pair16p", 64 << 10);
+    run<2, 8, 320>(in, n, out, probe, sms, ref, "pair16p");
   }
   return 0;
 }
