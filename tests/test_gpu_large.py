@@ -1,0 +1,93 @@
+"""GPU parity at BASELINE.json sizes through size-independent properties: full
+1 GiB streams against the oracle, closed-form counts for constant and sequential
+streams up to 8 GiB, sharded sums == whole stream, on-device generators == host
+generators, and the 64 x 16 MiB batch of the bench configuration chunk by chunk."""
+import numpy as np
+import pytest
+
+import paper_1011_0235_b200 as hs
+from paper_1011_0235_b200 import _native as N
+from paper_1011_0235_b200 import device as D
+from paper_1011_0235_b200.distributed import shard_range
+
+pytestmark = pytest.mark.gpu
+GiB = 1 << 30
+CHUNK = 16 << 20
+
+
+def dev_stream(cuda, spec):
+    buf = cuda.empty(spec.pixels, dtype=cuda.uint8, device="cuda")
+    hs.generate_device(spec, buf)
+    return buf
+
+
+@pytest.mark.parametrize("spec", [hs.SourceSpec("uniform", GiB, 5), hs.SourceSpec("normal", GiB, 6, mean=128.0, sigma=8.0)])
+def test_full_gib_against_oracle(cuda, oracle, spec):
+    buf = dev_stream(cuda, spec)
+    want = oracle.histogram(buf.cpu().numpy())
+    assert int(want.sum()) == GiB
+    pat = hs.compute_binning_pattern(hs.Histogram256(want))
+    for kind in (N.HS_KIND_NAIVE, N.HS_KIND_ADAPTIVE):
+        for impl in (N.HS_IMPL_LANE, N.HS_IMPL_WARP):
+            got = D.histograms([hs.DeviceChunk(buf)], kind, pat, impl)[0]
+            assert np.array_equal(got, want), (kind, impl)
+    del buf
+
+
+@pytest.mark.parametrize("gib", [1, 8])
+def test_closed_form_constant_and_sequential(cuda, gib):
+    n = gib * GiB
+    buf = cuda.empty(n, dtype=cuda.uint8, device="cuda")
+    for value in (0, 127, 255):
+        buf.fill_(value)
+        h = hs.naive_histogram(hs.DeviceChunk(buf), hs.WorkerGroupConfig())
+        assert h.counts[value] == n and h.total() == n
+        p = np.zeros(256, np.uint64)
+        p[value] = 1
+        a = hs.adaptive_histogram(hs.DeviceChunk(buf), hs.compute_binning_pattern(hs.Histogram256(p)), hs.WorkerGroupConfig())
+        assert a == h
+    hs.generate_device(hs.SourceSpec("sequential", n), buf)
+    h = hs.naive_histogram(hs.DeviceChunk(buf), hs.WorkerGroupConfig())
+    assert (h.counts == n // 256).all()
+    del buf
+
+
+def test_shards_sum_to_whole(cuda, oracle):
+    spec = hs.SourceSpec("normal", GiB + 4096 + 12, 9, mean=100.0, sigma=50.0)
+    buf = dev_stream(cuda, spec)
+    whole = hs.naive_histogram(hs.DeviceChunk(buf), hs.WorkerGroupConfig())
+    for world in (2, 4, 8):
+        parts = []
+        for r in range(world):
+            lo, hi = shard_range(spec.pixels, r, world)
+            parts.append(hs.naive_histogram(hs.DeviceChunk(buf[lo:hi]), hs.WorkerGroupConfig()))
+        assert hs.merge_all(parts) == whole
+    # each shard generated in place from its first pixel index equals the slice
+    lo, hi = shard_range(spec.pixels, 3, 8)
+    shard = cuda.empty(hi - lo, dtype=cuda.uint8, device="cuda")
+    hs.generate_device(spec, shard, lo)
+    assert bool((shard == buf[lo:hi]).all())
+    del buf
+
+
+def test_device_generator_matches_host_at_scale(cuda):
+    for spec in (hs.SourceSpec("normal", 64 << 20, 1011, mean=128.0, sigma=32.0),
+                 hs.SourceSpec("uniform", 256 << 20, 0xDEADBEEF)):
+        host = hs.generate(spec).pixels()
+        dev = dev_stream(cuda, spec)
+        assert np.array_equal(dev.cpu().numpy(), host), spec.kind
+
+
+def test_bench_configuration_per_chunk(cuda, oracle):
+    """64 x 16 MiB chunks of a sigma-32 stream in one ADAPTIVE launch (bench.py)."""
+    buf = cuda.empty(GiB, dtype=cuda.uint8, device="cuda")
+    for c in range(64):
+        hs.generate_device(hs.SourceSpec("normal", CHUNK, 0x10110235 ^ c, mean=128.0, sigma=32.0),
+                           buf[c * CHUNK:(c + 1) * CHUNK])
+    chunks = [hs.DeviceChunk(buf[c * CHUNK:(c + 1) * CHUNK]) for c in range(64)]
+    host = buf.cpu().numpy()
+    want = np.stack([oracle.histogram(host[c * CHUNK:(c + 1) * CHUNK]) for c in range(64)])
+    pat = hs.compute_binning_pattern(hs.Histogram256(want.sum(axis=0)))
+    got = hs.batch_histograms(chunks, hs.KernelKind.ADAPTIVE, pat, hs.WorkerGroupConfig())
+    assert np.array_equal(np.stack([g.counts for g in got]), want)
+    del buf
