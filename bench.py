@@ -269,6 +269,7 @@ def main(argv=None):
     pending: dict[int, tuple] = {}
     flip = [0, 0, 0]
     total_counts = torch.zeros(256, dtype=torch.int64, device=dev)
+    ws = torch.zeros(int(L.hs_workspace_bytes(64)), dtype=torch.uint8, device=dev)  # tickets + partials
     launch_events: list[tuple] = []
     dist_on = _dist_on()
 
@@ -286,7 +287,7 @@ def main(argv=None):
             e0.record(stream)
         st = L.hs_histogram_batched(streams[j].data_ptr(), N.u64p(begin), N.u64p(end), 64, N.HS_KIND_ADAPTIVE,
                                     N.HS_IMPL_AUTO, N.i64p(p.offset), N.i64p(p.count), 960, 8,
-                                    outs[j].data_ptr(), None, 0, stream.cuda_stream)
+                                    outs[j].data_ptr(), ws.data_ptr(), ws.numel(), stream.cuda_stream)
         N.check(st, "hs_histogram_batched")
         if record:
             e1 = torch.cuda.Event(enable_timing=True)

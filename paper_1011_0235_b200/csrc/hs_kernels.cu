@@ -110,9 +110,10 @@ __device__ __forceinline__ void for_each_piece(const SegParams& sp, Body&& body)
     if (s1 <= v) continue;
     const uint64_t hi = min(ve, s1);
     // sub-pieces of <= kCap bytes per CTA keep every narrow counter from wrapping
-    for (uint64_t a = v; a < hi; a += kCap) {
-      const uint64_t b = min(hi, a + kCap);
+    for (uint64_t a = v; a < hi;) {
+      const uint64_t b = (hi - a > kCap) ? a + kCap : hi;
       body(s, sp.begin[s] + (a - s0), sp.begin[s] + (b - s0));
+      a = b;
     }
     v = hi;
   }
@@ -201,24 +202,66 @@ constexpr int kLaneThreads = 1024;
 constexpr int kLaneMinBlocks = 2;
 constexpr uint32_t kLaneArrayBytes = 256 * 32 * 4;
 
-// Adds the CTA's counters into out[256] and re-zeroes them: 4 threads per bin, each
-// summing 8 of the bin's 32 lane words (staggered: conflict-free), shuffle-combined.
-__device__ __forceinline__ void lane_flush(uint32_t sbase, unsigned long long* __restrict__ out) {
+// Ticketed output (single launch, no memset): CTA c's counts for launch-local segment
+// s go to partial slot c + s (pieces are a monotone staircase over (CTA, segment), so
+// slots never collide); the last CTA to finish segment s (atomic ticket) sums the
+// slots of every CTA that touched it, stores out[s] and resets its ticket to zero.
+struct Tickets {
+  unsigned int* ticket;          // [kMaxSeg], zero on entry and on exit
+  unsigned long long* partial;   // [grid + nseg][256]
+};
+
+// CTA index owning word w of the balanced split (inverse of block_range)
+__device__ __forceinline__ uint32_t cta_of_word(uint64_t w, uint64_t tw, uint32_t g) {
+  const uint64_t q = tw / g, r = tw % g;
+  if (w < r * (q + 1)) return uint32_t(w / (q + 1));
+  return uint32_t(r + (w - r * (q + 1)) / q);
+}
+
+// Adds the CTA's counters into out[256] (or its partial slot) and re-zeroes them:
+// 4 threads per bin, each summing 8 of the bin's 32 lane words (staggered: conflict
+// free), shuffle-combined.
+__device__ __forceinline__ void lane_flush(uint32_t sbase, unsigned long long* __restrict__ out,
+                                           const Tickets& tk, const SegParams& sp, int s) {
   compiler_fence();
   __syncthreads();
+  const bool ticketed = tk.ticket != nullptr;
+  unsigned long long* dst = ticketed ? tk.partial + size_t(blockIdx.x + s) * 256 : out;
   for (uint32_t t = threadIdx.x; t < 1024; t += blockDim.x) {
     const uint32_t b = t >> 2, sub = t & 3;
-    uint32_t s = 0;
+    uint32_t v = 0;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const uint32_t a = sbase + b * 128 + (((sub * 8 + i + b) & 31) << 2);
-      s += sh_ld(a);
+      v += sh_ld(a);
       sh_st(a, 0);
     }
-    unsigned long long tot = s;
+    unsigned long long tot = v;
     tot += __shfl_xor_sync(0xffffffffu, tot, 1);
     tot += __shfl_xor_sync(0xffffffffu, tot, 2);
-    if (sub == 0 && tot) atomicAdd(out + b, tot);
+    if (sub == 0) {
+      if (ticketed) dst[b] = tot;
+      else if (tot) atomicAdd(out + b, tot);
+    }
+  }
+  if (ticketed) {
+    __shared__ unsigned int last;
+    __threadfence();
+    __syncthreads();
+    const uint64_t tw = sp.vstart[sp.nseg] >> 2;
+    const uint32_t c0 = cta_of_word(sp.vstart[s] >> 2, tw, gridDim.x);
+    const uint32_t c1 = cta_of_word((sp.vstart[s + 1] >> 2) - 1, tw, gridDim.x);
+    if (threadIdx.x == 0) last = (atomicAdd(tk.ticket + s, 1u) == c1 - c0) ? 1u : 0u;
+    __syncthreads();
+    if (last) {
+      __threadfence();
+      for (uint32_t b = threadIdx.x; b < 256; b += blockDim.x) {
+        unsigned long long tot = 0;
+        for (uint32_t c = c0; c <= c1; ++c) tot += __ldcg(tk.partial + size_t(c + s) * 256 + b);
+        out[b] = tot;
+      }
+      if (threadIdx.x == 0) tk.ticket[s] = 0;
+    }
   }
   compiler_fence();
   __syncthreads();
@@ -286,17 +329,25 @@ __device__ __noinline__ uint32_t lane_piece(const uint8_t* __restrict__ data, ui
 template <int U, bool HOT>
 __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
     k_lane(const uint8_t* __restrict__ data, const __grid_constant__ SegParams sp, int hot_bin,
-           unsigned long long* __restrict__ out) {
+           unsigned long long* __restrict__ out, Tickets tk) {
   __shared__ __align__(16) uint32_t counters[256 * 32];
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(counters);
   for (uint32_t i = threadIdx.x; i < kLaneArrayBytes / 16; i += blockDim.x) sh_st4(sbase + i * 16, make_uint4(0, 0, 0, 0));
   __syncthreads();
   const uint32_t tb = sbase + (threadIdx.x & 31) * 4;  // column base: bank == lane
   const uint32_t hot = uint32_t(hot_bin & 0xff);
-  for_each_piece<kBigCap>(sp, [&](int s, uint64_t p0, uint64_t p1) {
+  if (tk.ticket != nullptr && blockIdx.x == 0) {
+    // ticketed launches have no memset: CTA 0 zeroes the empty segments' outputs
+    for (int s = 0; s < sp.nseg; ++s)
+      if (sp.vstart[s + 1] == sp.vstart[s])
+        for (uint32_t b = threadIdx.x; b < 256; b += blockDim.x) out[size_t(sp.out_base + s) * 256 + b] = 0;
+  }
+  // u32 columns: a column adds at most (CTA bytes)/32 <= 2^32, so one flush per
+  // (CTA, segment) suffices -- required by the ticketed output
+  for_each_piece<~0ull>(sp, [&](int s, uint64_t p0, uint64_t p1) {
     const uint32_t hotcnt = lane_piece<U, HOT>(data, p0, p1, tb, hot * 0x01010101u);
     if (HOT && hotcnt) sh_add(tb + (hot << 7), hotcnt);
-    lane_flush(sbase, out + size_t(sp.out_base + s) * 256);
+    lane_flush(sbase, out + size_t(sp.out_base + s) * 256, tk, sp, s);
   });
 }
 
@@ -577,7 +628,7 @@ int set_smem(K kernel, size_t bytes) {
 // one launch over <= kMaxSeg segments
 int launch_batch(const uint8_t* d_data, const uint64_t* h_begin, const uint64_t* h_end, int s0, int ns,
                  int kind, int impl, const PatternParams* pp, unsigned long long* d_out, cudaStream_t st,
-                 const DevInfo& di) {
+                 const DevInfo& di, const Tickets& tk) {
   SegParams sp;
   sp.nseg = ns;
   sp.out_base = s0;
@@ -589,7 +640,6 @@ int launch_batch(const uint8_t* d_data, const uint64_t* h_begin, const uint64_t*
   }
   sp.vstart[ns] = v;
   if (v == 0) return HS_OK;
-  if (impl == HS_IMPL_AUTO) impl = HS_IMPL_LANE;
   cudaError_t e = cudaSuccess;
   if (impl == HS_IMPL_LANE) {
     // ~64 KiB of input per CTA at least; at most 2 resident CTAs per SM
@@ -597,9 +647,9 @@ int launch_batch(const uint8_t* d_data, const uint64_t* h_begin, const uint64_t*
     const int grid = int(std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(di.sms) * kLaneMinBlocks)));
     const int hb = pp ? pp->hot_bin : 0;
     if (kind == HS_KIND_ADAPTIVE)
-      k_lane<2, true><<<grid, kLaneThreads, 0, st>>>(d_data, sp, hb, d_out);
+      k_lane<2, true><<<grid, kLaneThreads, 0, st>>>(d_data, sp, hb, d_out, tk);
     else
-      k_lane<2, false><<<grid, kLaneThreads, 0, st>>>(d_data, sp, hb, d_out);
+      k_lane<2, false><<<grid, kLaneThreads, 0, st>>>(d_data, sp, hb, d_out, tk);
   } else if (impl == HS_IMPL_WARP) {
     const uint64_t want = (v + (32ull << 10) - 1) / (32ull << 10);
     const int grid = int(std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(di.sms) * 8)));
@@ -663,7 +713,14 @@ int hs_validate_pattern(const int64_t* h_offset, const int64_t* h_count, int64_t
   return validate(h_offset, h_count, total_slots, cap);
 }
 
-size_t hs_workspace_bytes(int nseg) { return nseg < 0 ? 0 : 256; }
+// [tickets: kMaxSeg u32][partials: (2*SMs + kMaxSeg) x 256 u64]; zero it once after
+// allocating -- every ticketed launch leaves the tickets at zero again.
+size_t hs_workspace_bytes(int nseg) {
+  if (nseg < 0) return 0;
+  DevInfo di;
+  if (dev_info(di) != HS_OK) return 0;
+  return 256 + size_t(kLaneMinBlocks * di.sms + kMaxSeg) * 256 * sizeof(uint64_t);
+}
 
 int hs_histogram_batched(const uint8_t* d_data, const uint64_t* h_begin, const uint64_t* h_end, int nseg,
                          int kind, int impl, const int64_t* h_offset, const int64_t* h_count,
@@ -690,16 +747,32 @@ int hs_histogram_batched(const uint8_t* d_data, const uint64_t* h_begin, const u
   if (reinterpret_cast<uintptr_t>(d_data) & 3) return HS_ERR_ALIGNMENT;
   if (nseg == 0) return HS_OK;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  cudaError_t e = cudaMemsetAsync(d_out, 0, size_t(nseg) * 256 * sizeof(uint64_t), st);
-  if (e != cudaSuccess) return fold(e);
-  if (total == 0) return HS_OK;
   DevInfo di;
   int rc = dev_info(di);
   if (rc != HS_OK) return rc;
+  if (impl == HS_IMPL_AUTO) impl = HS_IMPL_LANE;
+  // LANE with a workspace: one launch per <= 64 segments, output written in-kernel
+  Tickets tk{nullptr, nullptr};
+  const size_t need = 256 + size_t(kLaneMinBlocks * di.sms + kMaxSeg) * 256 * sizeof(uint64_t);
+  if (impl == HS_IMPL_LANE && d_ws != nullptr && ws_bytes >= need && total > 0) {
+    tk.ticket = reinterpret_cast<unsigned int*>(d_ws);
+    tk.partial = reinterpret_cast<unsigned long long*>(reinterpret_cast<uint8_t*>(d_ws) + 256);
+  } else {
+    cudaError_t e = cudaMemsetAsync(d_out, 0, size_t(nseg) * 256 * sizeof(uint64_t), st);
+    if (e != cudaSuccess) return fold(e);
+  }
+  if (total == 0) return HS_OK;
   for (int s0 = 0; s0 < nseg; s0 += kMaxSeg) {
     const int ns = std::min(kMaxSeg, nseg - s0);
+    bool empty = true;
+    for (int i = 0; i < ns; ++i) empty = empty && h_end[s0 + i] == h_begin[s0 + i];
+    if (empty && tk.ticket != nullptr) {
+      cudaError_t e = cudaMemsetAsync(d_out + size_t(s0) * 256, 0, size_t(ns) * 256 * sizeof(uint64_t), st);
+      if (e != cudaSuccess) return fold(e);
+      continue;
+    }
     rc = launch_batch(d_data, h_begin, h_end, s0, ns, kind, impl, have_pattern ? &pp : nullptr,
-                      reinterpret_cast<unsigned long long*>(d_out), st, di);
+                      reinterpret_cast<unsigned long long*>(d_out), st, di, tk);
     if (rc != HS_OK) return rc;
   }
   return HS_OK;

@@ -115,6 +115,7 @@ class Staging:
         self.device = t.device("cuda", t.cuda.current_device() if device is None else t.device(device).index)
         self._dev = None
         self._out_host = None
+        self._ws = None
 
     def device_bytes(self, n: int):
         t = torch()
@@ -123,6 +124,16 @@ class Staging:
             self._dev = t.empty(cap + 256, dtype=t.uint8, device=self.device)
         # 256-B aligned start (the allocator returns 512-B aligned blocks)
         return self._dev
+
+    def workspace(self):
+        """Device workspace of hs_histogram_batched (per-segment tickets + partials),
+        zeroed once; every launch leaves its tickets at zero again. Launches that
+        share it must be stream-ordered (one staging per stream user)."""
+        if self._ws is None:
+            t = torch()
+            n = int(N.lib().hs_workspace_bytes(64))
+            self._ws = t.zeros(max(n, 256), dtype=t.uint8, device=self.device)
+        return self._ws
 
     def host_out(self, nseg: int):
         t = torch()
@@ -206,11 +217,14 @@ def _pattern_args(pattern):
     return N.i64p(off), N.i64p(cnt), int(pattern.total_slots), int(pattern.cap), (off, cnt)
 
 
-def launch(staged: StagedBatch, kind: int, pattern=None, stream=None, impl: int = N.HS_IMPL_AUTO, out=None):
-    """hs_histogram_batched on ``stream`` (waits for the staging copies first).
-    Returns the device int64 tensor [nseg, 256] (counts, reinterpret as uint64)."""
+def launch(staged: StagedBatch, kind: int, pattern=None, stream=None, impl: int = N.HS_IMPL_AUTO, out=None,
+           staging: Staging | None = None):
+    """hs_histogram_batched on ``stream`` (waits for the staging copies first): one
+    kernel launch per <= 64 segments, output written in-kernel through ``staging``'s
+    workspace. Returns the device int64 tensor [nseg, 256] (reinterpret as uint64)."""
     t = require_cuda()
     stream = stream or t.cuda.current_stream()
+    ws = (staging or default_staging()).workspace()
     if staged.ready is not None:
         stream.wait_event(staged.ready)
     nseg = staged.nseg
@@ -222,7 +236,7 @@ def launch(staged: StagedBatch, kind: int, pattern=None, stream=None, impl: int 
     end = np.ascontiguousarray(staged.end, dtype=np.uint64)
     status = N.lib().hs_histogram_batched(
         staged.base or None, N.u64p(begin), N.u64p(end), nseg, int(kind), int(impl),
-        off_p, cnt_p, S, cap, out.data_ptr(), None, 0, stream.cuda_stream)
+        off_p, cnt_p, S, cap, out.data_ptr(), ws.data_ptr(), ws.numel(), stream.cuda_stream)
     N.check(status, "hs_histogram_batched")
     return out[:nseg] if nseg else out[:0]
 
@@ -263,7 +277,7 @@ def histograms(chunks: Sequence, kind: int, pattern=None, impl: int = N.HS_IMPL_
     stream = t.cuda.current_stream()
     st = default_staging()
     staged = stage(chunks, st, stream)
-    out = launch(staged, kind, pattern, stream, impl)
+    out = launch(staged, kind, pattern, stream, impl, staging=st)
     return readback(out, st, stream)
 
 

@@ -282,3 +282,36 @@ def test_concurrent_threads(cuda, oracle):
     for t in th:
         t.join()
     assert not errors
+
+
+def test_ticketed_output_matches_atomic_output(cuda, oracle):
+    """Single-launch path (workspace tickets, no memset) vs the memset + RED path of
+    the same ABI call, over ragged layouts: empty segments, tiny segments sharing a
+    CTA, segments spanning many CTAs, > 64 segments (several launches)."""
+    torch = cuda
+    L = N.lib()
+    rng = np.random.default_rng(77)
+    px = oracle.generate("normal", 64 << 20, 3, mean=128.0, sigma=20.0)
+    dev = torch.from_numpy(px).cuda()
+    ws = torch.zeros(int(L.hs_workspace_bytes(64)), dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream().cuda_stream
+    pat = hs.uniform_pattern(960)
+    for trial in range(12):
+        nseg = int(rng.integers(1, 150))
+        lens = rng.integers(0, (px.size // nseg) // 4 + 1, nseg) * 4
+        lens[rng.integers(0, nseg, max(1, nseg // 5))] = 0  # some empty segments
+        if trial % 3 == 0:
+            lens[:] = 4 * rng.integers(0, 64, nseg)  # tiny segments: many per CTA
+        begin = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.uint64)
+        end = begin + lens.astype(np.uint64)
+        want = np.stack([oracle.histogram(px[int(a):int(b)]) for a, b in zip(begin, end)])
+        for kind in (N.HS_KIND_NAIVE, N.HS_KIND_ADAPTIVE):
+            for use_ws in (True, False):
+                out = torch.full((nseg, 256), -1, dtype=torch.int64, device="cuda")
+                st = L.hs_histogram_batched(dev.data_ptr(), N.u64p(begin), N.u64p(end), nseg, kind, 0,
+                                            N.i64p(pat.offset), N.i64p(pat.count), 960, 8, out.data_ptr(),
+                                            ws.data_ptr() if use_ws else None, ws.numel() if use_ws else 0, stream)
+                N.check(st, "hs_histogram_batched")
+                assert np.array_equal(out.cpu().numpy().view(np.uint64), want), (trial, kind, use_ws)
+    # every launch leaves the tickets at zero
+    assert int(ws[:256].sum().item()) == 0
