@@ -202,13 +202,14 @@ constexpr int kLaneThreads = 1024;
 constexpr int kLaneMinBlocks = 2;
 constexpr uint32_t kLaneArrayBytes = 256 * 32 * 4;
 
-// Ticketed output (single launch, no memset): CTA c's counts for launch-local segment
-// s go to partial slot c + s (pieces are a monotone staircase over (CTA, segment), so
-// slots never collide); the last CTA to finish segment s (atomic ticket) sums the
-// slots of every CTA that touched it, stores out[s] and resets its ticket to zero.
+// Ticketed output (single launch, no memset): CTAs RED their counts for launch-local
+// segment s into a workspace accumulator row acc[s] that is zero between launches;
+// after a fence each CTA takes a ticket, and the last CTA to finish segment s takes
+// the row with atomicExch(.., 0) (reading and re-zeroing it), stores out[s] and
+// resets the ticket. Tail work is O(256) whatever the number of CTAs.
 struct Tickets {
   unsigned int* ticket;          // [kMaxSeg], zero on entry and on exit
-  unsigned long long* partial;   // [grid + nseg][256]
+  unsigned long long* acc;       // [kMaxSeg][256], zero on entry and on exit
 };
 
 // CTA index owning word w of the balanced split (inverse of block_range)
@@ -218,15 +219,15 @@ __device__ __forceinline__ uint32_t cta_of_word(uint64_t w, uint64_t tw, uint32_
   return uint32_t(r + (w - r * (q + 1)) / q);
 }
 
-// Adds the CTA's counters into out[256] (or its partial slot) and re-zeroes them:
-// 4 threads per bin, each summing 8 of the bin's 32 lane words (staggered: conflict
-// free), shuffle-combined.
+// Adds the CTA's counters into out[256] (or the segment's accumulator row) and
+// re-zeroes them: 4 threads per bin, each summing 8 of the bin's 32 lane words
+// (staggered: conflict free), shuffle-combined.
 __device__ __forceinline__ void lane_flush(uint32_t sbase, unsigned long long* __restrict__ out,
                                            const Tickets& tk, const SegParams& sp, int s) {
   compiler_fence();
   __syncthreads();
   const bool ticketed = tk.ticket != nullptr;
-  unsigned long long* dst = ticketed ? tk.partial + size_t(blockIdx.x + s) * 256 : out;
+  unsigned long long* dst = ticketed ? tk.acc + size_t(s) * 256 : out;
   for (uint32_t t = threadIdx.x; t < 1024; t += blockDim.x) {
     const uint32_t b = t >> 2, sub = t & 3;
     uint32_t v = 0;
@@ -239,27 +240,22 @@ __device__ __forceinline__ void lane_flush(uint32_t sbase, unsigned long long* _
     unsigned long long tot = v;
     tot += __shfl_xor_sync(0xffffffffu, tot, 1);
     tot += __shfl_xor_sync(0xffffffffu, tot, 2);
-    if (sub == 0) {
-      if (ticketed) dst[b] = tot;
-      else if (tot) atomicAdd(out + b, tot);
-    }
+    if (sub == 0 && tot) atomicAdd(dst + b, tot);
   }
   if (ticketed) {
     __shared__ unsigned int last;
     __threadfence();
     __syncthreads();
-    const uint64_t tw = sp.vstart[sp.nseg] >> 2;
-    const uint32_t c0 = cta_of_word(sp.vstart[s] >> 2, tw, gridDim.x);
-    const uint32_t c1 = cta_of_word((sp.vstart[s + 1] >> 2) - 1, tw, gridDim.x);
-    if (threadIdx.x == 0) last = (atomicAdd(tk.ticket + s, 1u) == c1 - c0) ? 1u : 0u;
+    if (threadIdx.x == 0) {
+      const uint64_t tw = sp.vstart[sp.nseg] >> 2;
+      const uint32_t c0 = cta_of_word(sp.vstart[s] >> 2, tw, gridDim.x);
+      const uint32_t c1 = cta_of_word((sp.vstart[s + 1] >> 2) - 1, tw, gridDim.x);
+      last = (atomicAdd(tk.ticket + s, 1u) == c1 - c0) ? 1u : 0u;
+    }
     __syncthreads();
     if (last) {
       __threadfence();
-      for (uint32_t b = threadIdx.x; b < 256; b += blockDim.x) {
-        unsigned long long tot = 0;
-        for (uint32_t c = c0; c <= c1; ++c) tot += __ldcg(tk.partial + size_t(c + s) * 256 + b);
-        out[b] = tot;
-      }
+      for (uint32_t b = threadIdx.x; b < 256; b += blockDim.x) out[b] = atomicExch(dst + b, 0ull);
       if (threadIdx.x == 0) tk.ticket[s] = 0;
     }
   }
@@ -713,14 +709,10 @@ int hs_validate_pattern(const int64_t* h_offset, const int64_t* h_count, int64_t
   return validate(h_offset, h_count, total_slots, cap);
 }
 
-// [tickets: kMaxSeg u32][partials: (2*SMs + kMaxSeg) x 256 u64]; zero it once after
-// allocating -- every ticketed launch leaves the tickets at zero again.
-size_t hs_workspace_bytes(int nseg) {
-  if (nseg < 0) return 0;
-  DevInfo di;
-  if (dev_info(di) != HS_OK) return 0;
-  return 256 + size_t(kLaneMinBlocks * di.sms + kMaxSeg) * 256 * sizeof(uint64_t);
-}
+// [tickets: kMaxSeg u32, padded to 256 B][accumulators: kMaxSeg x 256 u64]; zero it once
+// after allocating -- every ticketed launch leaves it zero again.
+constexpr size_t kWorkspaceBytes = 256 + size_t(kMaxSeg) * 256 * sizeof(uint64_t);
+size_t hs_workspace_bytes(int nseg) { return nseg < 0 ? 0 : kWorkspaceBytes; }
 
 int hs_histogram_batched(const uint8_t* d_data, const uint64_t* h_begin, const uint64_t* h_end, int nseg,
                          int kind, int impl, const int64_t* h_offset, const int64_t* h_count,
@@ -753,10 +745,9 @@ int hs_histogram_batched(const uint8_t* d_data, const uint64_t* h_begin, const u
   if (impl == HS_IMPL_AUTO) impl = HS_IMPL_LANE;
   // LANE with a workspace: one launch per <= 64 segments, output written in-kernel
   Tickets tk{nullptr, nullptr};
-  const size_t need = 256 + size_t(kLaneMinBlocks * di.sms + kMaxSeg) * 256 * sizeof(uint64_t);
-  if (impl == HS_IMPL_LANE && d_ws != nullptr && ws_bytes >= need && total > 0) {
+  if (impl == HS_IMPL_LANE && d_ws != nullptr && ws_bytes >= kWorkspaceBytes && total > 0) {
     tk.ticket = reinterpret_cast<unsigned int*>(d_ws);
-    tk.partial = reinterpret_cast<unsigned long long*>(reinterpret_cast<uint8_t*>(d_ws) + 256);
+    tk.acc = reinterpret_cast<unsigned long long*>(reinterpret_cast<uint8_t*>(d_ws) + 256);
   } else {
     cudaError_t e = cudaMemsetAsync(d_out, 0, size_t(nseg) * 256 * sizeof(uint64_t), st);
     if (e != cudaSuccess) return fold(e);

@@ -313,5 +313,5 @@ def test_ticketed_output_matches_atomic_output(cuda, oracle):
                                             ws.data_ptr() if use_ws else None, ws.numel() if use_ws else 0, stream)
                 N.check(st, "hs_histogram_batched")
                 assert np.array_equal(out.cpu().numpy().view(np.uint64), want), (trial, kind, use_ws)
-    # every launch leaves the tickets at zero
-    assert int(ws[:256].sum().item()) == 0
+    # every launch leaves the workspace (tickets and accumulator rows) zero again
+    assert int(ws.sum().item()) == 0
