@@ -76,7 +76,7 @@ int hs_device_query(int device, int* sm_count, int* smem_optin, int* l2_bytes);
 int hs_validate_pattern(const int64_t* h_offset, const int64_t* h_count,
                         int64_t total_slots, int64_t cap);
 
-/* Device workspace needed by hs_histogram_batched for `nseg` segments. */
+/* Device workspace of hs_histogram_batched / hs_stream_step (tickets + accumulator rows). */
 size_t hs_workspace_bytes(int nseg);
 
 /*
@@ -89,7 +89,12 @@ size_t hs_workspace_bytes(int nseg);
  *   impl     HS_IMPL_* (HS_IMPL_AUTO for production)
  *   h_offset/h_count: the CPU binning pattern (pattern.py:94-133), may be NULL
  *            for NAIVE; validated before launch (kernels.py:363).
- *   d_out    uint64[nseg*256], overwritten (zeroed by the call on `stream`).
+ *   d_out    uint64[nseg*256], overwritten.
+ *   d_ws     optional workspace of hs_workspace_bytes() bytes, zeroed once by the caller:
+ *            the call is then ONE kernel launch per <= 64 segments (CTAs RED into
+ *            workspace rows; the last CTA per segment stores d_out and re-zeroes its row).
+ *            Without it a memset of d_out precedes the launch. Calls sharing a workspace
+ *            must be stream-ordered.
  * Byte offsets must be multiples of 4 (PackedChunk words, core.py:38-67).
  */
 int hs_histogram_batched(const uint8_t* d_data, const uint64_t* h_begin, const uint64_t* h_end,
@@ -128,6 +133,27 @@ int hs_ablation_stage(const uint8_t* d_data, uint64_t n_bytes, int stage,
                       int64_t total_slots, int64_t cap,
                       uint64_t* d_sink, uint64_t* d_out256, void* d_ws, size_t ws_bytes,
                       void* stream);
+
+/* ---- device-resident stream engine ----------------------------------------
+ * The accumulator, moving window and NVHist/AHist switch of the stream driver
+ * (stream.py:62-116, :390-425; policy.py:39-64) kept on the device, so lag-1 kernel
+ * switching runs at device speed with no host round trip.
+ * State is caller-allocated (hs_stream_state_bytes) and zeroed by hs_stream_reset. */
+size_t hs_stream_state_bytes(int window_size);
+int hs_stream_reset(void* d_state, int window_size, void* stream);
+
+/* One iteration: histograms of the batch's nseg (<= 64) segments into d_out[nseg][256]
+ * with the kernel kind and hot bin the previous fold decided (read on the device), then
+ * the fold: acc += each chunk, window push/evict (error bit on NegativeCount),
+ * d_kind_log[iteration] = kind used, d_deg_log[iteration] = window degeneracy,
+ * d_div_log[iteration] = total-variation(acc, window) in numpy's summation order, and
+ * -- when (iteration+1) % recompute_every == 0 -- the decision for the next iteration:
+ * ADAPTIVE iff degeneracy >= threshold (policy.py:49-53), hot bin = window argmax.
+ * Requires a workspace of hs_workspace_bytes(). Asynchronous; no host sync. */
+int hs_stream_step(const uint8_t* d_data, const uint64_t* h_begin, const uint64_t* h_end, int nseg,
+                   void* d_state, int window_size, double threshold, int recompute_every, int iteration,
+                   uint64_t* d_out, double* d_deg_log, double* d_div_log, int32_t* d_kind_log,
+                   void* d_ws, size_t ws_bytes, void* stream);
 
 /* ---- host-side control plane (native replacements of pattern.py / policy.py) */
 

@@ -68,6 +68,9 @@ EXPORTED = (
     "hs_degeneracy",
     "hs_generate_host",
     "hs_generate_device",
+    "hs_stream_state_bytes",
+    "hs_stream_reset",
+    "hs_stream_step",
 )
 
 _c = ctypes
@@ -108,6 +111,13 @@ _SIGNATURES = {
     "hs_generate_device": (
         _c.c_int,
         [_c.c_int, _U64, _c.c_int, _c.c_double, _c.c_double, _U64, _P, _U64, _P],
+    ),
+    "hs_stream_state_bytes": (_c.c_size_t, [_c.c_int]),
+    "hs_stream_reset": (_c.c_int, [_P, _c.c_int, _P]),
+    "hs_stream_step": (
+        _c.c_int,
+        [_P, _U64P, _U64P, _c.c_int, _P, _c.c_int, _c.c_double, _c.c_int, _c.c_int, _P, _P, _P, _P, _P,
+         _c.c_size_t, _P],
     ),
 }
 

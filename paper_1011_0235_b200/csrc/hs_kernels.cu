@@ -268,7 +268,7 @@ __device__ __forceinline__ void lane_flush(uint32_t sbase, unsigned long long* _
 // Returns the thread's register count of all-hot vectors (ADAPTIVE).
 template <int U, bool HOT>
 __device__ __noinline__ uint32_t lane_piece(const uint8_t* __restrict__ data, uint64_t p0, uint64_t p1,
-                                            uint32_t tb, uint32_t hot4) {
+                                            uint32_t tb, uint32_t hot4, bool hot_on) {
   constexpr uint32_t T = kLaneThreads;
   const uint32_t tid = threadIdx.x;
   uint32_t hotcnt = 0;
@@ -281,7 +281,7 @@ __device__ __noinline__ uint32_t lane_piece(const uint8_t* __restrict__ data, ui
   // ADAPTIVE counts 16-B vectors made only of the CPU pattern's hot bin in a register
   // (no shared-memory traffic for degenerate input).
   auto vec = [&](const uint4& v) {
-    if (HOT) {
+    if (HOT && hot_on) {
       const uint32_t d = (v.x ^ hot4) | (v.y ^ hot4) | (v.z ^ hot4) | (v.w ^ hot4);
       if (d == 0) { hotcnt += 16; return; }
     }
@@ -325,13 +325,19 @@ __device__ __noinline__ uint32_t lane_piece(const uint8_t* __restrict__ data, ui
 template <int U, bool HOT>
 __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
     k_lane(const uint8_t* __restrict__ data, const __grid_constant__ SegParams sp, int hot_bin,
-           unsigned long long* __restrict__ out, Tickets tk) {
+           unsigned long long* __restrict__ out, Tickets tk, const uint32_t* __restrict__ decision) {
   __shared__ __align__(16) uint32_t counters[256 * 32];
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(counters);
   for (uint32_t i = threadIdx.x; i < kLaneArrayBytes / 16; i += blockDim.x) sh_st4(sbase + i * 16, make_uint4(0, 0, 0, 0));
   __syncthreads();
   const uint32_t tb = sbase + (threadIdx.x & 31) * 4;  // column base: bank == lane
-  const uint32_t hot = uint32_t(hot_bin & 0xff);
+  // device-resident stream engine: {kind, hot bin} decided by the previous fold on the GPU
+  bool hot_on = HOT;
+  uint32_t hot = uint32_t(hot_bin & 0xff);
+  if (decision != nullptr) {
+    hot_on = HOT && __ldcg(decision) == uint32_t(HS_KIND_ADAPTIVE);
+    hot = __ldcg(decision + 1) & 0xff;
+  }
   if (tk.ticket != nullptr && blockIdx.x == 0) {
     // ticketed launches have no memset: CTA 0 zeroes the empty segments' outputs
     for (int s = 0; s < sp.nseg; ++s)
@@ -341,7 +347,7 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
   // u32 columns: a column adds at most (CTA bytes)/32 <= 2^32, so one flush per
   // (CTA, segment) suffices -- required by the ticketed output
   for_each_piece<~0ull>(sp, [&](int s, uint64_t p0, uint64_t p1) {
-    const uint32_t hotcnt = lane_piece<U, HOT>(data, p0, p1, tb, hot * 0x01010101u);
+    const uint32_t hotcnt = lane_piece<U, HOT>(data, p0, p1, tb, hot * 0x01010101u, hot_on);
     if (HOT && hotcnt) sh_add(tb + (hot << 7), hotcnt);
     lane_flush(sbase, out + size_t(sp.out_base + s) * 256, tk, sp, s);
   });
@@ -516,6 +522,115 @@ __global__ void __launch_bounds__(kSubThreads)
   if (tot) atomicAdd(out + b, tot);
 }
 
+// ================================================================== device stream engine
+// Device-resident accumulator, moving window and switch policy (stream.py:62-116,
+// :390-425; policy.py:39-64) so lag-1 kernel switching needs no host round trip.
+// State (caller-allocated, hs_stream_state_bytes): header | acc[256] | win[256] | ring[W][256].
+struct DevStreamHeader {
+  uint32_t kind;   // kernel kind for the next launch (read by k_lane through `decision`)
+  uint32_t hot;    // hot bin for ADAPTIVE: argmax of the window (lowest bin on ties)
+  uint32_t head;   // ring head
+  uint32_t count;  // ring entries
+  uint32_t error;  // 1: NegativeCount (stream.py:96-97), 2: empty totals
+  uint32_t pad0[3];
+  unsigned long long chunks_seen;
+  unsigned long long pad1[3];
+};
+static_assert(sizeof(DevStreamHeader) == 64, "header size");
+
+// numpy's float64 add.reduce over a contiguous array (pairwise, 8 accumulators, blocks
+// of 128): reproduces np.abs(pa - pb).sum() bit for bit (numpy 2.3, checked on 20k cases)
+__device__ double np_pairwise_sum(const double* a, int n) {
+  if (n < 8) {
+    double r = 0.0;
+    for (int i = 0; i < n; ++i) r = __dadd_rn(r, a[i]);
+    return r;
+  }
+  if (n <= 128) {
+    double r[8];
+    for (int j = 0; j < 8; ++j) r[j] = a[j];
+    int i = 8;
+    for (; i < n - (n % 8); i += 8)
+      for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a[i + j]);
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (; i < n; ++i) res = __dadd_rn(res, a[i]);
+    return res;
+  }
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  return __dadd_rn(np_pairwise_sum(a, n2), np_pairwise_sum(a + n2, n - n2));
+}
+
+__global__ void __launch_bounds__(256)
+    k_stream_fold(const unsigned long long* __restrict__ hist, int nseg, uint8_t* __restrict__ state, int window,
+                  double threshold, int decide, int iteration, double* __restrict__ deg_log,
+                  double* __restrict__ div_log, int32_t* __restrict__ kind_log) {
+  DevStreamHeader* hd = reinterpret_cast<DevStreamHeader*>(state);
+  unsigned long long* acc = reinterpret_cast<unsigned long long*>(state + sizeof(DevStreamHeader));
+  unsigned long long* win = acc + 256;
+  unsigned long long* ring = win + 256;
+  __shared__ unsigned long long sa[256], sw[256];
+  __shared__ double d[256];
+  __shared__ unsigned int err;
+  __shared__ unsigned long long ta_s, tb_s;
+  const int b = threadIdx.x;
+  if (b == 0) err = 0;
+  __syncthreads();
+  uint32_t head = hd->head, count = hd->count;
+  unsigned long long a = acc[b], w = win[b];
+  for (int j = 0; j < nseg; ++j) {  // push each chunk in order (stream.py:_StreamState.post)
+    const unsigned long long h = hist[size_t(j) * 256 + b];
+    a += h;
+    if (count < uint32_t(window)) {
+      ring[size_t((head + count) % window) * 256 + b] = h;
+      w += h;
+      ++count;
+    } else {
+      const unsigned long long old = ring[size_t(head) * 256 + b];
+      w += h;
+      if (w < old) atomicOr(&err, 1u);
+      w -= old;
+      ring[size_t(head) * 256 + b] = h;
+      head = (head + 1) % window;
+    }
+  }
+  acc[b] = a;
+  win[b] = w;
+  sa[b] = a;
+  sw[b] = w;
+  __syncthreads();
+  if (b == 0) {
+    unsigned long long ta = 0, tb = 0, mx = 0;
+    uint32_t am = 0;
+    for (int i = 0; i < 256; ++i) {
+      ta += sa[i];
+      tb += sw[i];
+      if (sw[i] > mx) { mx = sw[i]; am = i; }  // np.argmax: first maximum
+    }
+    const double frac = tb ? __ddiv_rn((double)mx, (double)tb) : 0.0;
+    deg_log[iteration] = frac;
+    kind_log[iteration] = int32_t(hd->kind);
+    ta_s = ta;
+    tb_s = tb;
+    if (decide) {  // decision for the next iteration (lag 1)
+      hd->kind = frac >= threshold ? HS_KIND_ADAPTIVE : HS_KIND_NAIVE;
+      hd->hot = am;
+    }
+    hd->head = head;
+    hd->count = count;
+    hd->chunks_seen += uint64_t(nseg);
+    if (err) hd->error |= 1u;
+    if (ta == 0 || tb == 0) hd->error |= 2u;
+  }
+  __syncthreads();
+  const double pa = ta_s ? __ddiv_rn((double)sa[b], (double)ta_s) : 0.0;
+  const double pb = tb_s ? __ddiv_rn((double)sw[b], (double)tb_s) : 0.0;
+  d[b] = fabs(__dadd_rn(pa, -pb));
+  __syncthreads();
+  if (b == 0) div_log[iteration] = __dmul_rn(0.5, np_pairwise_sum(d, 256));
+}
+
 // ================================================================== generators
 __host__ __device__ __forceinline__ uint64_t sm64_mix(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -624,7 +739,7 @@ int set_smem(K kernel, size_t bytes) {
 // one launch over <= kMaxSeg segments
 int launch_batch(const uint8_t* d_data, const uint64_t* h_begin, const uint64_t* h_end, int s0, int ns,
                  int kind, int impl, const PatternParams* pp, unsigned long long* d_out, cudaStream_t st,
-                 const DevInfo& di, const Tickets& tk) {
+                 const DevInfo& di, const Tickets& tk, const uint32_t* decision = nullptr) {
   SegParams sp;
   sp.nseg = ns;
   sp.out_base = s0;
@@ -642,10 +757,10 @@ int launch_batch(const uint8_t* d_data, const uint64_t* h_begin, const uint64_t*
     const uint64_t want = (v + (64ull << 10) - 1) / (64ull << 10);
     const int grid = int(std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(di.sms) * kLaneMinBlocks)));
     const int hb = pp ? pp->hot_bin : 0;
-    if (kind == HS_KIND_ADAPTIVE)
-      k_lane<2, true><<<grid, kLaneThreads, 0, st>>>(d_data, sp, hb, d_out, tk);
+    if (kind == HS_KIND_ADAPTIVE || decision != nullptr)
+      k_lane<2, true><<<grid, kLaneThreads, 0, st>>>(d_data, sp, hb, d_out, tk, decision);
     else
-      k_lane<2, false><<<grid, kLaneThreads, 0, st>>>(d_data, sp, hb, d_out, tk);
+      k_lane<2, false><<<grid, kLaneThreads, 0, st>>>(d_data, sp, hb, d_out, tk, nullptr);
   } else if (impl == HS_IMPL_WARP) {
     const uint64_t want = (v + (32ull << 10) - 1) / (32ull << 10);
     const int grid = int(std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(di.sms) * 8)));
@@ -843,6 +958,56 @@ int hs_ablation_stage(const uint8_t* d_data, uint64_t n_bytes, int stage, const 
   k_ablation<<<grid, kSubThreads, smem, st>>>(d_data, n_bytes, stage, pp,
                                                reinterpret_cast<unsigned long long*>(d_sink),
                                                reinterpret_cast<unsigned long long*>(d_out256));
+  return fold(cudaGetLastError());
+}
+
+size_t hs_stream_state_bytes(int window_size) {
+  if (window_size < 1) return 0;
+  return sizeof(DevStreamHeader) + size_t(2 + window_size) * 256 * sizeof(uint64_t);
+}
+
+int hs_stream_reset(void* d_state, int window_size, void* stream) {
+  if (!d_state || window_size < 1) return HS_ERR_INVALID_ARG;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  return fold(cudaMemsetAsync(d_state, 0, hs_stream_state_bytes(window_size), st));  // kind NAIVE, hot 0
+}
+
+int hs_stream_step(const uint8_t* d_data, const uint64_t* h_begin, const uint64_t* h_end, int nseg,
+                   void* d_state, int window_size, double threshold, int recompute_every, int iteration,
+                   uint64_t* d_out, double* d_deg_log, double* d_div_log, int32_t* d_kind_log,
+                   void* d_ws, size_t ws_bytes, void* stream) {
+  if (!d_state || window_size < 1 || nseg < 1 || nseg > kMaxSeg || recompute_every < 1 || iteration < 0 ||
+      !d_out || !d_deg_log || !d_div_log || !d_kind_log || !h_begin || !h_end)
+    return HS_ERR_INVALID_ARG;
+  if (!(threshold > 0.0 && threshold < 1.0)) return HS_ERR_INVALID_ARG;
+  if (!d_ws || ws_bytes < kWorkspaceBytes) return HS_ERR_WORKSPACE;
+  uint64_t total = 0;
+  for (int s = 0; s < nseg; ++s) {
+    if ((h_begin[s] & 3) || (h_end[s] & 3) || h_end[s] < h_begin[s]) return HS_ERR_ALIGNMENT;
+    total += h_end[s] - h_begin[s];
+  }
+  if (reinterpret_cast<uintptr_t>(d_data) & 3) return HS_ERR_ALIGNMENT;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  DevInfo di;
+  int rc = dev_info(di);
+  if (rc != HS_OK) return rc;
+  Tickets tk{reinterpret_cast<unsigned int*>(d_ws),
+             reinterpret_cast<unsigned long long*>(reinterpret_cast<uint8_t*>(d_ws) + 256)};
+  bool empty = total == 0;
+  if (empty) {
+    cudaError_t e = cudaMemsetAsync(d_out, 0, size_t(nseg) * 256 * sizeof(uint64_t), st);
+    if (e != cudaSuccess) return fold(e);
+  } else {
+    rc = launch_batch(d_data, h_begin, h_end, 0, nseg, HS_KIND_NAIVE, HS_IMPL_LANE, nullptr,
+                      reinterpret_cast<unsigned long long*>(d_out), st, di, tk,
+                      reinterpret_cast<const uint32_t*>(d_state));
+    if (rc != HS_OK) return rc;
+  }
+  // pattern and kernel refresh for iteration+1 when (iteration+1) % every == 0 (stream.py:407-414)
+  const int decide = ((iteration + 1) % recompute_every) == 0;
+  k_stream_fold<<<1, 256, 0, st>>>(reinterpret_cast<const unsigned long long*>(d_out), nseg,
+                                   reinterpret_cast<uint8_t*>(d_state), window_size, threshold, decide, iteration,
+                                   d_deg_log, d_div_log, d_kind_log);
   return fold(cudaGetLastError());
 }
 

@@ -165,3 +165,47 @@ def test_device_resident_stream(cuda, oracle):
     want = [oracle.histogram(oracle.generate("normal", px, 77 ^ i, mean=128.0, sigma=32.0)) for i in range(n_chunks)]
     assert [h[0].counts.tolist() for h in rep.per_slice_histograms] == [w.tolist() for w in want]
     assert acc.running.counts.tolist() == np.sum(want, axis=0).tolist()
+
+
+def _device_batches(torch, segments, batch_size):
+    for batch in schedule_stream(segments, batch_size):
+        yield [hs.DeviceChunk(torch.from_numpy(c.pixels().copy()).cuda()) for c in batch]
+
+
+def test_device_stream_matches_reference(cuda, golden):
+    """hs_stream_step (fold + policy on the device) reproduces the reference's own
+    run_sequential: kernel log, per-slice histograms, accumulator, window ring and the
+    float degeneracy/divergence logs, bit for bit."""
+    for i, m in enumerate(golden.meta["streams"]):
+        cfg = hs.PipelineConfig(num_iterations=m["num_iterations"], chunk_pixels=m["chunk_pixels"],
+                                batch_size=m["batch_size"], recompute_pattern_every=m["recompute_pattern_every"],
+                                window_size=m["window_size"], worker=hs.WorkerGroupConfig(4, 2))
+        acc, win, rep, log = hs.run_device_stream(_device_batches(cuda, _segments(m), m["batch_size"]), cfg, POLICY)
+        assert [k.value for k in log] == m["kernel_log"], i
+        per = np.stack([np.stack([h.counts for h in it]) for it in rep.per_slice_histograms])
+        assert np.array_equal(per, golden[f"stream_{i}_per_slice"])
+        assert np.array_equal(acc.running.counts, golden[f"stream_{i}_acc"]) and acc.chunks_seen == m["chunks_seen"]
+        assert np.array_equal(win.windowed.counts, golden[f"stream_{i}_window"])
+        assert np.array_equal(np.stack([h.counts for h in win.ring]), golden[f"stream_{i}_ring"])
+        assert rep.degeneracy_log == golden[f"stream_{i}_deg"].tolist(), i
+        assert rep.divergence_log == golden[f"stream_{i}_div"].tolist(), i
+
+
+def test_device_stream_equals_host_engine_at_scale(cuda):
+    """16 MiB chunks (the C2/C3 configuration): normal sigma 8 -> mixture -> constant, so
+    the on-device switch flips NAIVE -> ADAPTIVE mid-stream; equal to run_sequential."""
+    px = 1 << 24
+    segs = [(hs.SourceSpec("normal", px, 3, mean=128.0, sigma=8.0), 4),
+            (hs.SourceSpec("mixture", px, 3, value=200, degeneracy=0.9), 3),
+            (hs.SourceSpec("constant", px, 3, value=127), 3)]
+    cfg = hs.PipelineConfig(num_iterations=10, chunk_pixels=px, window_size=2)
+    seq = hs.run_sequential(schedule_stream(segs), cfg, POLICY)
+    dev = hs.run_device_stream(_device_batches(cuda, segs, 1), cfg, POLICY)
+    assert states_equal(seq, dev)
+    assert hs.KernelKind.ADAPTIVE in dev[3] and dev[3][0] is hs.KernelKind.NAIVE
+
+
+def test_device_stream_rejects_host_chunks(cuda):
+    cfg = small_cfg(num_iterations=2)
+    with pytest.raises(TypeError):
+        hs.run_device_stream(uniform_source(cfg, 1), cfg, POLICY)
