@@ -241,20 +241,23 @@ def launch(staged: StagedBatch, kind: int, pattern=None, stream=None, impl: int 
     return out[:nseg] if nseg else out[:0]
 
 
-def readback(out_dev, staging: Staging | None = None, stream=None) -> np.ndarray:
-    """D2H of [n, 256] counts (pinned, async) then wait; returns uint64 numpy (a copy)."""
+def readback(out_dev, staging: Staging | None = None, stream=None, timed: bool = False):
+    """D2H of [n, 256] counts (pinned, async) then wait; returns uint64 numpy (a copy).
+    With ``timed`` also returns the timing-enabled completion event."""
     t = torch()
     stream = stream or t.cuda.current_stream()
     n = out_dev.shape[0]
     if n == 0:
-        return np.zeros((0, BINS), np.uint64)
+        res = np.zeros((0, BINS), np.uint64)
+        return (res, None) if timed else res
     host = staging.host_out(n) if staging is not None else t.empty(n * BINS, dtype=t.int64, pin_memory=True)
     with t.cuda.stream(stream):
         host.view(n, BINS).copy_(out_dev, non_blocking=True)
-        ev = t.cuda.Event()
+        ev = t.cuda.Event(enable_timing=timed)
         ev.record(stream)
     ev.synchronize()
-    return host.numpy().reshape(n, BINS).view(np.uint64).copy()
+    res = host.numpy().reshape(n, BINS).view(np.uint64).copy()
+    return (res, ev) if timed else res
 
 
 _local = threading.local()
