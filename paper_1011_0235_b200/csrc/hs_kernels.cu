@@ -47,6 +47,7 @@ struct PatternParams {
   uint32_t entry[256];           // offset | count << 16   (sub-bin kernels)
   int32_t total_slots;
   int32_t hot_bin;               // ADAPTIVE hot bin (argmax count, lowest bin on ties)
+  int32_t hot_unique;            // exactly one bin holds the maximal count: a dominant value
 };
 
 // ------------------------------------------------------------------ primitives
@@ -199,6 +200,7 @@ __device__ __forceinline__ EachVec<U, VecFn> each_vec(VecFn& f) { return EachVec
 // Per byte: PRMT (extract) + IMAD (address) + ATOMS.POPC.INC.
 // A column (lane) adds at most piece/32 per flush; pieces are capped at 1 GiB per CTA.
 constexpr int kLaneThreads = 1024;
+constexpr int kLaneHotThreads = 768;
 constexpr int kLaneMinBlocks = 2;
 constexpr uint32_t kLaneArrayBytes = 256 * 32 * 4;
 
@@ -222,8 +224,8 @@ __device__ __forceinline__ uint32_t cta_of_word(uint64_t w, uint64_t tw, uint32_
 // Adds the CTA's counters into out[256] (or the segment's accumulator row) and
 // re-zeroes them: 4 threads per bin, each summing 8 of the bin's 32 lane words
 // (staggered: conflict free), shuffle-combined.
-__device__ __forceinline__ void lane_flush(uint32_t sbase, unsigned long long* __restrict__ out,
-                                           const Tickets& tk, const SegParams& sp, int s) {
+__device__ __noinline__ void lane_flush(uint32_t sbase, unsigned long long* __restrict__ out,
+                                        const Tickets& tk, const SegParams& sp, int s) {
   compiler_fence();
   __syncthreads();
   const bool ticketed = tk.ticket != nullptr;
@@ -265,11 +267,10 @@ __device__ __forceinline__ void lane_flush(uint32_t sbase, unsigned long long* _
 
 // The streaming loop of one piece, written lean for the 32-register budget of 64
 // resident warps: 32-bit vector counts, a running 16-B pointer, compile-time stride.
-// Returns the thread's register count of all-hot vectors (ADAPTIVE).
-template <int U, bool HOT>
-__device__ __noinline__ uint32_t lane_piece(const uint8_t* __restrict__ data, uint64_t p0, uint64_t p1,
-                                            uint32_t tb, uint32_t hot4, bool hot_on) {
-  constexpr uint32_t T = kLaneThreads;
+template <int U, bool HOT, int TH>
+__device__ __forceinline__ uint32_t lane_loop(const uint8_t* __restrict__ data, uint64_t a0, uint64_t a1,
+                                              uint32_t tb, uint32_t hot4) {
+  constexpr uint32_t T = TH;
   const uint32_t tid = threadIdx.x;
   uint32_t hotcnt = 0;
   auto word = [&](uint32_t w) {
@@ -278,22 +279,15 @@ __device__ __noinline__ uint32_t lane_piece(const uint8_t* __restrict__ data, ui
     sh_inc(tb + (byte_of(w, 2) << 7));
     sh_inc(tb + (byte_of(w, 3) << 7));
   };
-  // ADAPTIVE counts 16-B vectors made only of the CPU pattern's hot bin in a register
-  // (no shared-memory traffic for degenerate input).
   auto vec = [&](const uint4& v) {
-    if (HOT && hot_on) {
+    if (HOT) {  // a 16-B vector made only of the hot bin is counted in a register
       const uint32_t d = (v.x ^ hot4) | (v.y ^ hot4) | (v.z ^ hot4) | (v.w ^ hot4);
       if (d == 0) { hotcnt += 16; return; }
     }
     word(v.x); word(v.y); word(v.z); word(v.w);
   };
-  const uint64_t base = reinterpret_cast<uintptr_t>(data);
-  const uint64_t a0 = min(p1, ((base + p0 + 15) & ~uint64_t(15)) - base);
-  const uint64_t a1 = max(a0, ((base + p1) & ~uint64_t(15)) - base);
-  if (p0 + 4ull * tid < a0) word(*reinterpret_cast<const uint32_t*>(data + p0 + 4ull * tid));
-  if (a1 + 4ull * tid < p1) word(*reinterpret_cast<const uint32_t*>(data + a1 + 4ull * tid));
   const uint4* __restrict__ q = reinterpret_cast<const uint4*>(data + a0) + tid;
-  const uint32_t nv = uint32_t((a1 - a0) >> 4);  // pieces are <= 1 GiB
+  const uint32_t nv = uint32_t((a1 - a0) >> 4);  // pieces are < 2^36 bytes
   const uint32_t nfull = nv / (U * T);
   uint4 A[U], B[U];
   if (nfull > 0) {
@@ -322,8 +316,37 @@ __device__ __noinline__ uint32_t lane_piece(const uint8_t* __restrict__ data, ui
   return hotcnt;
 }
 
-template <int U, bool HOT>
-__global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
+// One piece [p0, p1): unaligned head/tail words, then the 16-B body. Compiled as its
+// own function so the segment walk around it does not take its registers. HOT
+// (ADAPTIVE) tests every vector against the CPU pattern's hot bin and adds the
+// register count of hot bytes to the thread's column at the end.
+// (Tried and rejected: verifying the hot bin on a per-CTA sample and switching between
+// the checked and the plain loop at run time -- both loops in one function exceed the
+// 32-register budget of 64 resident warps and the plain loop spills.)
+template <int U, bool HOT, int TH>
+__device__ __noinline__ uint32_t lane_piece(const uint8_t* __restrict__ data, uint64_t p0, uint64_t p1,
+                                            uint32_t tb, uint32_t hot4) {
+  const uint32_t tid = threadIdx.x;
+  auto word = [&](uint32_t w) {
+    sh_inc(tb + (byte_of(w, 0) << 7));
+    sh_inc(tb + (byte_of(w, 1) << 7));
+    sh_inc(tb + (byte_of(w, 2) << 7));
+    sh_inc(tb + (byte_of(w, 3) << 7));
+  };
+  const uint64_t base = reinterpret_cast<uintptr_t>(data);
+  const uint64_t a0 = min(p1, ((base + p0 + 15) & ~uint64_t(15)) - base);
+  const uint64_t a1 = max(a0, ((base + p1) & ~uint64_t(15)) - base);
+  if (p0 + 4ull * tid < a0) word(*reinterpret_cast<const uint32_t*>(data + p0 + 4ull * tid));
+  if (a1 + 4ull * tid < p1) word(*reinterpret_cast<const uint32_t*>(data + a1 + 4ull * tid));
+  const uint32_t hotcnt = lane_loop<U, HOT, TH>(data, a0, a1, tb, hot4);
+  if (HOT && hotcnt) sh_add(tb + ((hot4 & 0xffu) << 7), hotcnt);
+  return 0;
+}
+
+// HOT (ADAPTIVE): register path for the hot bin `hot_bin`; with `decision` (device
+// stream engine) the hot bin comes from the previous fold on the device.
+template <int U, bool HOT, int TH = kLaneThreads>
+__global__ void __launch_bounds__(TH, kLaneMinBlocks)
     k_lane(const uint8_t* __restrict__ data, const __grid_constant__ SegParams sp, int hot_bin,
            unsigned long long* __restrict__ out, Tickets tk, const uint32_t* __restrict__ decision) {
   __shared__ __align__(16) uint32_t counters[256 * 32];
@@ -332,12 +355,7 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
   __syncthreads();
   const uint32_t tb = sbase + (threadIdx.x & 31) * 4;  // column base: bank == lane
   // device-resident stream engine: {kind, hot bin} decided by the previous fold on the GPU
-  bool hot_on = HOT;
-  uint32_t hot = uint32_t(hot_bin & 0xff);
-  if (decision != nullptr) {
-    hot_on = HOT && __ldcg(decision) == uint32_t(HS_KIND_ADAPTIVE);
-    hot = __ldcg(decision + 1) & 0xff;
-  }
+  const uint32_t hot = (decision != nullptr ? __ldcg(decision + 1) : uint32_t(hot_bin)) & 0xff;
   if (tk.ticket != nullptr && blockIdx.x == 0) {
     // ticketed launches have no memset: CTA 0 zeroes the empty segments' outputs
     for (int s = 0; s < sp.nseg; ++s)
@@ -346,9 +364,9 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
   }
   // u32 columns: a column adds at most (CTA bytes)/32 <= 2^32, so one flush per
   // (CTA, segment) suffices -- required by the ticketed output
+  const uint32_t hot4 = hot * 0x01010101u;
   for_each_piece<~0ull>(sp, [&](int s, uint64_t p0, uint64_t p1) {
-    const uint32_t hotcnt = lane_piece<U, HOT>(data, p0, p1, tb, hot * 0x01010101u, hot_on);
-    if (HOT && hotcnt) sh_add(tb + (hot << 7), hotcnt);
+    lane_piece<U, HOT, TH>(data, p0, p1, tb, hot4);
     lane_flush(sbase, out + size_t(sp.out_base + s) * 256, tk, sp, s);
   });
 }
@@ -720,12 +738,17 @@ int make_pattern(const int64_t* off, const int64_t* cnt, int64_t S, int64_t cap,
   if (st != HS_OK) return st;
   if (S > 65535) return HS_ERR_UNSUPPORTED;
   int64_t best = -1;
+  int nbest = 0;
   pp.hot_bin = 0;
   for (int b = 0; b < 256; ++b) {
     const int64_t c = cnt[b] > 0xffff ? 0xffff : cnt[b];
     pp.entry[b] = uint32_t(off[b]) | (uint32_t(c) << 16);
-    if (cnt[b] > best) { best = cnt[b]; pp.hot_bin = b; }
+    if (cnt[b] > best) { best = cnt[b]; pp.hot_bin = b; nbest = 1; }
+    else if (cnt[b] == best) ++nbest;
   }
+  // The apportionment gives a dominant value the unique widest run; a spread prior
+  // (normal, uniform) ties many bins at the cap or leaves all below it.
+  pp.hot_unique = nbest == 1 && best > 1;
   pp.total_slots = int32_t(S);
   return HS_OK;
 }
@@ -757,8 +780,13 @@ int launch_batch(const uint8_t* d_data, const uint64_t* h_begin, const uint64_t*
     const uint64_t want = (v + (64ull << 10) - 1) / (64ull << 10);
     const int grid = int(std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(di.sms) * kLaneMinBlocks)));
     const int hb = pp ? pp->hot_bin : 0;
-    if (kind == HS_KIND_ADAPTIVE || decision != nullptr)
-      k_lane<2, true><<<grid, kLaneThreads, 0, st>>>(d_data, sp, hb, d_out, tk, decision);
+    // ADAPTIVE runs the register path for the pattern's hot bin only when the pattern
+    // marks a dominant value (unique widest sub-bin run): its per-vector test costs ~2%
+    // on spread data and gains on degenerate data. The HOT form uses 768-thread CTAs
+    // (40 registers): at 1024 threads its loop spills under the 32-register budget.
+    // The device stream engine always runs the HOT form (its kind is decided on the GPU).
+    if (decision != nullptr || (kind == HS_KIND_ADAPTIVE && pp != nullptr && pp->hot_unique))
+      k_lane<2, true, kLaneHotThreads><<<grid, kLaneHotThreads, 0, st>>>(d_data, sp, hb, d_out, tk, decision);
     else
       k_lane<2, false><<<grid, kLaneThreads, 0, st>>>(d_data, sp, hb, d_out, tk, nullptr);
   } else if (impl == HS_IMPL_WARP) {

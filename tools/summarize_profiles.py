@@ -73,7 +73,7 @@ def full(tag, report, command):
     rd = float(vals[hdr.index("dram__bytes_read.sum")].replace(",", "")) * SCALE[units[hdr.index("dram__bytes_read.sum")]]
     wr = float(vals[hdr.index("dram__bytes_write.sum")].replace(",", "")) * SCALE[units[hdr.index("dram__bytes_write.sum")]]
     (ROOT / "profiles" / "traffic.json").write_text(json.dumps({
-        "k_lane_adaptive_bytes_per_launch": rd + wr, "algorithmic_bytes_per_launch": 1 << 30,
+        "k_lane_bytes_per_launch": rd + wr, "algorithmic_bytes_per_launch": 1 << 30,
         "source": f"profiles/{out.name} (dram__bytes_read.sum + dram__bytes_write.sum)"}, indent=1) + "\n")
     return out
 
