@@ -74,6 +74,8 @@ class ClockSampler:
 
     def __init__(self, index: int):
         self.samples: list[int] = []
+        self.mem_samples: list[int] = []
+        self.power: list[float] = []
         self.reasons = 0
         self.max_mhz = None
         self._stop = threading.Event()
@@ -91,6 +93,8 @@ class ClockSampler:
         while not self._stop.is_set():
             try:
                 self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.mem_samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_MEM))
+                self.power.append(self.nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0)
                 self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
             except Exception:
                 pass
@@ -112,7 +116,9 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
         reasons = [n for bit, n in self.NAMES.items() if self.reasons & bit and bit != 0x1]
         return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
-                "reasons": reasons, "samples": len(self.samples)}
+                "reasons": reasons, "samples": len(self.samples),
+                "mem_mhz": float(statistics.median(self.mem_samples)) if self.mem_samples else None,
+                "power_w_max": round(max(self.power), 1) if self.power else None}
 
 
 # ----------------------------------------------------------------------- distributed
@@ -234,6 +240,7 @@ def main(argv=None):
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extras", action="store_true")
     args = ap.parse_args(argv)
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -317,8 +324,40 @@ def main(argv=None):
             for sj in side:
                 sj.wait_stream(stream)
 
+    def serial_roofline():
+        # ---- roofline: the same launches (same patterns), back to back on one stream, all
+        # enqueued before the first completes (the queue never drains): per-sigma average
+        # launch duration = CUDA-event time of 10 consecutive launches / 10. (In the timed
+        # region kernels overlap across the sigma streams, so per-launch events there would
+        # include waiting behind the neighbour kernel.)
+        s0 = side[0]
+        s0.wait_stream(stream)
+        reps = 10
+        per_sigma = {}
+        ev = []
+        torch.cuda._sleep(50_000_000)
+        for j in range(len(SIGMAS)):
+            p = patterns[j]
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(s0)
+            for _ in range(reps):
+                N.check(L.hs_histogram_batched(streams[j].data_ptr(), N.u64p(begin), N.u64p(end), 64, N.HS_KIND_ADAPTIVE,
+                                               N.HS_IMPL_AUTO, N.i64p(p.offset), N.i64p(p.count), 960, 8,
+                                               outs[j].data_ptr(), wss[0].data_ptr(), wss[0].numel(), s0.cuda_stream),
+                        "hs_histogram_batched")
+            b.record(s0)
+            ev.append((j, a, b))
+        torch.cuda.synchronize()
+        for j, a, b in ev:
+            per_sigma[f"sigma{int(SIGMAS[j])}"] = round(a.elapsed_time(b) / reps, 4)
+        launch_ms = list(per_sigma.values())
+        avg_launch_ms = float(np.mean(launch_ms))
+        return per_sigma, launch_ms, avg_launch_ms, reps
+
     for _ in range(args.warmup):
         step()
+    torch.cuda.synchronize()
+    per_sigma, launch_ms, avg_launch_ms, reps = serial_roofline()
     torch.cuda.synchronize()
     barrier(world)
     torch.cuda.synchronize()
@@ -336,33 +375,10 @@ def main(argv=None):
         torch.cuda.synchronize()
     barrier(world)
     elapsed_ms = max_over_ranks(t0.elapsed_time(t1), world)
+    if os.environ.get("HS_BENCH_DEBUG"):
+        print("serial before timed region:", per_sigma, "after:", serial_roofline()[0], file=sys.stderr)
     bytes_per_step_rank = len(SIGMAS) * GiB
     value = world * bytes_per_step_rank * args.steps / (elapsed_ms / 1e3) / 1e9
-
-    # ---- roofline: the same launches (same patterns) serially on one stream, all enqueued
-    # before the first completes so the queue never drains and each event pair brackets
-    # only its kernel (in the timed region kernels overlap across the sigma streams)
-    serial_steps = min(args.steps, 20)
-    s0 = side[0]
-    s0.wait_stream(stream)
-    pairs = []
-    for _ in range(serial_steps):
-        for j in range(len(SIGMAS)):
-            p = patterns[j]
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(s0)
-            N.check(L.hs_histogram_batched(streams[j].data_ptr(), N.u64p(begin), N.u64p(end), 64, N.HS_KIND_ADAPTIVE,
-                                           N.HS_IMPL_AUTO, N.i64p(p.offset), N.i64p(p.count), 960, 8,
-                                           outs[j].data_ptr(), wss[0].data_ptr(), wss[0].numel(), s0.cuda_stream),
-                    "hs_histogram_batched")
-            e1.record(s0)
-            pairs.append((j, e0, e1))
-    torch.cuda.synchronize()
-    launch_ms = [a.elapsed_time(b) for _, a, b in pairs]
-    avg_launch_ms = float(np.mean(launch_ms[len(SIGMAS):]))  # first step warms the queue
-    per_sigma_ms = {f"sigma{int(SIGMAS[j])}": round(float(np.mean([a.elapsed_time(b) for jj, a, b in pairs[len(SIGMAS):] if jj == j])), 4)
-                    for j in range(len(SIGMAS))}
 
     # ---- correctness spot check of the last step against closed-form totals
     for j in range(len(SIGMAS)):
@@ -383,7 +399,7 @@ def main(argv=None):
             traffic = None
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
-                "achieved_method": f"1 GiB / mean CUDA-event duration of {len(launch_ms) - len(SIGMAS)} serial launches on one stream",
+                "achieved_method": "1 GiB / mean launch duration (CUDA events around 10 back-to-back launches per sigma stream, after warm-up, before the timed region)",
                 "concurrent_streams_gbs": round(value / world, 1),
                 "kernel": "k_lane, kind ADAPTIVE (hs_histogram_batched, 64 x 16 MiB segments; per-launch events on its stream)",
                 "algorithmic_bytes_per_launch": GiB}
@@ -396,6 +412,11 @@ def main(argv=None):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(streams, args.cpu_seconds)
+
+    extra = {}
+    if rank == 0 and not args.no_extras:
+        extra["c1_image_1024x1024"] = c1_image(hs, N, torch, L, dev)
+        extra["c3_switch_stream"] = c3_switch(hs, torch, dev)
 
     if rank == 0:
         line = {
@@ -411,13 +432,126 @@ def main(argv=None):
             "e2e": e2e,
             "gpu_launches": len(SIGMAS) * args.steps,  # k_lane launches in the timed region
             "clocks": clocks.summary(),
-            "per_launch_ms": {"mean": round(avg_launch_ms, 4), "min": round(min(launch_ms), 4),
-                              "max": round(max(launch_ms), 4), "serial_launches": len(launch_ms), **per_sigma_ms},
+            "per_launch_ms": {"mean": round(avg_launch_ms, 4), "back_to_back_launches": reps * len(SIGMAS), **per_sigma},
+            **extra,
         }
         print(json.dumps(line), flush=True)
     if _dist_on():
         torch.distributed.destroy_process_group()
     return 0
+
+
+def c1_image(hs, N, torch, L, dev):
+    """BASELINE configs[0]: one 1024x1024 uniform image (seed 0). L2-resident and
+    launch-bound, so reported beside the headline: latency through the public API,
+    64 images per launch, and single-image launches replayed from a CUDA graph."""
+    from oracle import oracle as O
+
+    n = 1 << 20
+    spec = hs.SourceSpec("uniform", n, 0)
+    chunk = hs.generate(spec)
+    want = O.histogram(chunk.pixels())
+    cfg = hs.WorkerGroupConfig()
+    for _ in range(5):
+        h = hs.naive_histogram(chunk, cfg)
+    assert np.array_equal(h.counts, want)
+    t0 = time.perf_counter()
+    for _ in range(50):
+        hs.naive_histogram(chunk, cfg)
+    api_us = (time.perf_counter() - t0) / 50 * 1e6
+    # 64 images, one launch
+    imgs = torch.empty(64 * n, dtype=torch.uint8, device=dev)
+    for i in range(64):
+        hs.generate_device(hs.SourceSpec("uniform", n, i), imgs[i * n:(i + 1) * n])
+    b0 = (np.arange(64, dtype=np.uint64) * n)
+    b1 = b0 + n
+    out = torch.empty((64, 256), dtype=torch.int64, device=dev)
+    ws = torch.zeros(int(L.hs_workspace_bytes(64)), dtype=torch.uint8, device=dev)
+    s = torch.cuda.current_stream()
+
+    def batched():
+        N.check(L.hs_histogram_batched(imgs.data_ptr(), N.u64p(b0), N.u64p(b1), 64, N.HS_KIND_NAIVE, 0, None, None,
+                                       0, 0, out.data_ptr(), ws.data_ptr(), ws.numel(), s.cuda_stream), "batched")
+
+    for _ in range(3):
+        batched()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda._sleep(20_000_000)
+    a.record()
+    for _ in range(20):
+        batched()
+    b.record()
+    b.synchronize()
+    batch_us = a.elapsed_time(b) / 20 * 1e3
+    # single-image launches captured in a CUDA graph
+    one0, one1 = np.zeros(1, np.uint64), np.full(1, n, np.uint64)
+    out1 = torch.empty((1, 256), dtype=torch.int64, device=dev)
+    g = torch.cuda.CUDAGraph()
+    cs = torch.cuda.Stream()
+    cs.wait_stream(s)
+    with torch.cuda.stream(cs):
+        N.check(L.hs_histogram_batched(imgs.data_ptr(), N.u64p(one0), N.u64p(one1), 1, N.HS_KIND_NAIVE, 0, None, None,
+                                       0, 0, out1.data_ptr(), ws.data_ptr(), ws.numel(), cs.cuda_stream), "warm")
+    s.wait_stream(cs)
+    with torch.cuda.graph(g):
+        gs = torch.cuda.current_stream()
+        for _ in range(100):
+            N.check(L.hs_histogram_batched(imgs.data_ptr(), N.u64p(one0), N.u64p(one1), 1, N.HS_KIND_NAIVE, 0, None,
+                                           None, 0, 0, out1.data_ptr(), ws.data_ptr(), ws.numel(), gs.cuda_stream),
+                    "capture")
+    g.replay()
+    torch.cuda.synchronize()
+    a.record()
+    g.replay()
+    b.record()
+    b.synchronize()
+    graph_us = a.elapsed_time(b) / 100 * 1e3
+    assert np.array_equal(out1[0].cpu().numpy().view(np.uint64), O.histogram(imgs[:n].cpu().numpy()))
+    t0 = time.perf_counter()
+    for _ in range(5):
+        O.naive_histogram(chunk.words, 32, host_cores())
+    cpu_us = (time.perf_counter() - t0) / 5 * 1e6
+    return {"bytes": n, "public_api_us_per_image": round(api_us, 2),
+            "batched_64_images_us_per_image": round(batch_us / 64, 3),
+            "batched_64_images_gbs": round(64 * n / (batch_us * 1e3), 1),
+            "graph_single_image_us": round(graph_us, 3), "cpu_reference_port_us": round(cpu_us, 1)}
+
+
+def c3_switch(hs, torch, dev):
+    """BASELINE configs[2]: a stream that turns degenerate (uniform -> mixture p=0.9 ->
+    constant 127), 16 MiB chunks, 16 chunks per iteration, through the device-resident
+    engine: per-iteration lag-1 NVHist/AHist switching decided on the GPU."""
+    px, per_iter = CHUNK, 16
+    segs = [("uniform", {}), ("mixture", {"value": 127, "degeneracy": 0.9}), ("constant", {"value": 127})]
+    iters_per_seg = 2
+    total = len(segs) * iters_per_seg * per_iter
+    buf = torch.empty(total * px, dtype=torch.uint8, device=dev)
+    k = 0
+    for kind, kw in segs:
+        for _ in range(iters_per_seg * per_iter):
+            sl = buf[k * px:(k + 1) * px]
+            if kind == "mixture":
+                sl.copy_(torch.from_numpy(hs.generate(hs.SourceSpec(kind, px, k, **kw)).pixels().copy()))
+            else:
+                hs.generate_device(hs.SourceSpec(kind, px, k, **kw), sl)
+            k += 1
+    iters = total // per_iter
+    cfg = hs.PipelineConfig(num_iterations=iters, chunk_pixels=px, batch_size=per_iter, window_size=1)
+
+    def src():
+        for i in range(iters):
+            yield [hs.DeviceChunk(buf[(i * per_iter + j) * px:(i * per_iter + j + 1) * px]) for j in range(per_iter)]
+
+    hs.run_device_stream(src(), cfg, hs.SwitchPolicy())
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    acc, _, rep, log = hs.run_device_stream(src(), cfg, hs.SwitchPolicy())
+    wall = time.perf_counter() - t0
+    assert acc.running.total() == total * px
+    dev_ns = sum(s.compute_ns for s in rep.stages)
+    return {"bytes": total * px, "chunks": total, "iterations": iters,
+            "device_gbs": round(total * px / dev_ns, 1), "wall_gbs": round(total * px / wall / 1e9, 1),
+            "kernel_log": [k.value for k in log], "degeneracy_log": [round(d, 4) for d in rep.degeneracy_log]}
 
 
 def e2e_run(hs, D, torch, streams, world, steps):

@@ -83,6 +83,12 @@ __device__ __forceinline__ void sh_st4(uint32_t addr, uint4 v) {
 
 __device__ __forceinline__ void compiler_fence() { asm volatile("" ::: "memory"); }
 
+// Programmatic dependent launch (no-ops unless launched with the PDL attribute):
+// let the next kernel on the stream start filling SMs as this one's CTAs retire, and
+// wait for the previous kernel to finish before touching memory it may still use.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // byte k of w, zero-extended (PRMT)
 __device__ __forceinline__ uint32_t byte_of(uint32_t w, int k) { return __byte_perm(w, 0u, 0x4440u | k); }
 
@@ -228,6 +234,7 @@ __device__ __noinline__ void lane_flush(uint32_t sbase, unsigned long long* __re
                                         const Tickets& tk, const SegParams& sp, int s) {
   compiler_fence();
   __syncthreads();
+  pdl_wait();  // the previous launch on this stream may still own the workspace / outputs
   const bool ticketed = tk.ticket != nullptr;
   unsigned long long* dst = ticketed ? tk.acc + size_t(s) * 256 : out;
   for (uint32_t t = threadIdx.x; t < 1024; t += blockDim.x) {
@@ -356,11 +363,17 @@ __global__ void __launch_bounds__(TH, kLaneMinBlocks)
   const uint32_t tb = sbase + (threadIdx.x & 31) * 4;  // column base: bank == lane
   // device-resident stream engine: {kind, hot bin} decided by the previous fold on the GPU
   const uint32_t hot = (decision != nullptr ? __ldcg(decision + 1) : uint32_t(hot_bin)) & 0xff;
+  pdl_launch_dependents();  // the next launch's CTAs may take SMs as ours retire
   if (tk.ticket != nullptr && blockIdx.x == 0) {
     // ticketed launches have no memset: CTA 0 zeroes the empty segments' outputs
-    for (int s = 0; s < sp.nseg; ++s)
-      if (sp.vstart[s + 1] == sp.vstart[s])
-        for (uint32_t b = threadIdx.x; b < 256; b += blockDim.x) out[size_t(sp.out_base + s) * 256 + b] = 0;
+    bool any_empty = false;
+    for (int s = 0; s < sp.nseg; ++s) any_empty |= sp.vstart[s + 1] == sp.vstart[s];
+    if (any_empty) {
+      pdl_wait();
+      for (int s = 0; s < sp.nseg; ++s)
+        if (sp.vstart[s + 1] == sp.vstart[s])
+          for (uint32_t b = threadIdx.x; b < 256; b += blockDim.x) out[size_t(sp.out_base + s) * 256 + b] = 0;
+    }
   }
   // u32 columns: a column adds at most (CTA bytes)/32 <= 2^32, so one flush per
   // (CTA, segment) suffices -- required by the ticketed output
@@ -785,10 +798,24 @@ int launch_batch(const uint8_t* d_data, const uint64_t* h_begin, const uint64_t*
     // on spread data and gains on degenerate data. The HOT form uses 768-thread CTAs
     // (40 registers): at 1024 threads its loop spills under the 32-register budget.
     // The device stream engine always runs the HOT form (its kind is decided on the GPU).
-    if (decision != nullptr || (kind == HS_KIND_ADAPTIVE && pp != nullptr && pp->hot_unique))
-      k_lane<2, true, kLaneHotThreads><<<grid, kLaneHotThreads, 0, st>>>(d_data, sp, hb, d_out, tk, decision);
-    else
-      k_lane<2, false><<<grid, kLaneThreads, 0, st>>>(d_data, sp, hb, d_out, tk, nullptr);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    // PDL overlaps a launch's ramp with the previous launch's tail; the device stream
+    // engine's launches stay fully ordered (they read the previous fold's decision)
+    cfg.attrs = decision == nullptr ? attr : nullptr;
+    cfg.numAttrs = decision == nullptr ? 1 : 0;
+    if (decision != nullptr || (kind == HS_KIND_ADAPTIVE && pp != nullptr && pp->hot_unique)) {
+      cfg.blockDim = dim3(kLaneHotThreads);
+      e = cudaLaunchKernelEx(&cfg, k_lane<2, true, kLaneHotThreads>, d_data, sp, hb, d_out, tk, decision);
+    } else {
+      cfg.blockDim = dim3(kLaneThreads);
+      e = cudaLaunchKernelEx(&cfg, k_lane<2, false>, d_data, sp, hb, d_out, tk, (const uint32_t*)nullptr);
+    }
+    if (e != cudaSuccess) return fold(e);
   } else if (impl == HS_IMPL_WARP) {
     const uint64_t want = (v + (32ull << 10) - 1) / (32ull << 10);
     const int grid = int(std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(di.sms) * 8)));
