@@ -138,7 +138,10 @@ int hs_ablation_stage(const uint8_t* d_data, uint64_t n_bytes, int stage,
  * The accumulator, moving window and NVHist/AHist switch of the stream driver
  * (stream.py:62-116, :390-425; policy.py:39-64) kept on the device, so lag-1 kernel
  * switching runs at device speed with no host round trip.
- * State is caller-allocated (hs_stream_state_bytes) and zeroed by hs_stream_reset. */
+ * State is caller-allocated (hs_stream_state_bytes) and zeroed by hs_stream_reset.
+ * Error word: uint32 at byte offset 16 of the state, sticky, read once after the last
+ * step -- bit 0 = window count went negative (stream.py NegativeCount), bit 1 = empty
+ * histogram in divergence (policy.py EmptyHistogram). */
 size_t hs_stream_state_bytes(int window_size);
 int hs_stream_reset(void* d_state, int window_size, void* stream);
 

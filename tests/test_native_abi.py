@@ -84,3 +84,24 @@ def test_missing_library_fails_loudly(monkeypatch, tmp_path):
     with pytest.raises(N.NativeLibraryError):
         N.lib()
     monkeypatch.setattr(N, "_lib", None)
+
+
+def test_stream_engine_abi_validation():
+    """hs_stream_* reject bad arguments before any device work."""
+    lib = N.lib()
+    assert lib.hs_stream_state_bytes(0) == 0
+    assert lib.hs_stream_state_bytes(4) == 64 + (2 + 4) * 256 * 8
+    assert lib.hs_stream_reset(None, 4, None) == N.HS_ERR_INVALID_ARG
+    b = np.zeros(1, np.uint64)
+    e = np.full(1, 8, np.uint64)
+    p = ctypes.c_void_p(256)  # never dereferenced: validation fails first
+    step = lib.hs_stream_step
+    ws_need = lib.hs_workspace_bytes(64)
+    # nseg out of range, threshold outside (0, 1), missing workspace
+    assert step(p, N.u64p(b), N.u64p(e), 0, p, 4, 0.45, 1, 0, p, p, p, p, p, ws_need, None) == N.HS_ERR_INVALID_ARG
+    assert step(p, N.u64p(b), N.u64p(e), 65, p, 4, 0.45, 1, 0, p, p, p, p, p, ws_need, None) == N.HS_ERR_INVALID_ARG
+    assert step(p, N.u64p(b), N.u64p(e), 1, p, 4, 1.0, 1, 0, p, p, p, p, p, ws_need, None) == N.HS_ERR_INVALID_ARG
+    assert step(p, N.u64p(b), N.u64p(e), 1, p, 4, 0.45, 0, 0, p, p, p, p, p, ws_need, None) == N.HS_ERR_INVALID_ARG
+    assert step(p, N.u64p(b), N.u64p(e), 1, p, 4, 0.45, 1, 0, p, p, p, p, None, 0, None) == N.HS_ERR_WORKSPACE
+    e6 = np.full(1, 6, np.uint64)
+    assert step(p, N.u64p(b), N.u64p(e6), 1, p, 4, 0.45, 1, 0, p, p, p, p, p, ws_need, None) == N.HS_ERR_ALIGNMENT
