@@ -89,6 +89,22 @@ __device__ __forceinline__ void compiler_fence() { asm volatile("" ::: "memory")
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// Instrumented builds only (-DHS_TRACE, tools/trace_lane.py): thread 0 of each k_lane
+// CTA stamps %globaltimer at fixed points of its life; compiled out otherwise.
+#ifdef HS_TRACE
+__device__ unsigned long long hs_trace_buf[1024][16];
+#define HS_STAMP(slot)                                                                          \
+  do {                                                                                          \
+    if (threadIdx.x == 0 && blockIdx.x < 1024 && (slot) < 16) {                                 \
+      unsigned long long t_;                                                                    \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                    \
+      hs_trace_buf[blockIdx.x][(slot)] = t_;                                                    \
+    }                                                                                           \
+  } while (0)
+#else
+#define HS_STAMP(slot) do { } while (0)
+#endif
+
 // byte k of w, zero-extended (PRMT)
 __device__ __forceinline__ uint32_t byte_of(uint32_t w, int k) { return __byte_perm(w, 0u, 0x4440u | k); }
 
@@ -227,16 +243,16 @@ __device__ __forceinline__ uint32_t cta_of_word(uint64_t w, uint64_t tw, uint32_
   return uint32_t(r + (w - r * (q + 1)) / q);
 }
 
-// Adds the CTA's counters into out[256] (or the segment's accumulator row) and
-// re-zeroes them: 4 threads per bin, each summing 8 of the bin's 32 lane words
-// (staggered: conflict free), shuffle-combined.
-__device__ __noinline__ void lane_flush(uint32_t sbase, unsigned long long* __restrict__ out,
-                                        const Tickets& tk, const SegParams& sp, int s) {
+// Adds the CTA's counters into dst[256] (the output row, or the segment's accumulator
+// row of a ticketed launch) and re-zeroes them: 4 threads per bin, each summing 8 of
+// the bin's 32 lane words (staggered: conflict free), shuffle-combined. No fence here:
+// a mid-range flush must not wait for its REDs to reach L2 (that round trip under a
+// saturated memory system was ~6 us per CTA; tools/ab_seg.py), so the fence and the
+// tickets are taken once per CTA at the end (lane_tickets).
+__device__ __noinline__ void lane_flush(uint32_t sbase, unsigned long long* __restrict__ dst) {
   compiler_fence();
   __syncthreads();
   pdl_wait();  // the previous launch on this stream may still own the workspace / outputs
-  const bool ticketed = tk.ticket != nullptr;
-  unsigned long long* dst = ticketed ? tk.acc + size_t(s) * 256 : out;
   for (uint32_t t = threadIdx.x; t < 1024; t += blockDim.x) {
     const uint32_t b = t >> 2, sub = t & 3;
     uint32_t v = 0;
@@ -251,25 +267,42 @@ __device__ __noinline__ void lane_flush(uint32_t sbase, unsigned long long* __re
     tot += __shfl_xor_sync(0xffffffffu, tot, 2);
     if (sub == 0 && tot) atomicAdd(dst + b, tot);
   }
-  if (ticketed) {
-    __shared__ unsigned int last;
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const uint64_t tw = sp.vstart[sp.nseg] >> 2;
+  compiler_fence();
+  __syncthreads();
+}
+
+// End of a ticketed CTA that flushed segments [s_first, s_last] into their accumulator
+// rows: one fence, then a ticket per segment; the last CTA of a segment takes the row
+// with atomicExch(.., 0) (reading and re-zeroing it), stores the output row and resets
+// the ticket, so workspace and tickets are zero again when the launch ends.
+__device__ __noinline__ void lane_tickets(const Tickets& tk, const SegParams& sp, int s_first, int s_last,
+                                          unsigned long long* __restrict__ out) {
+  __shared__ unsigned long long lastmask;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint64_t tw = sp.vstart[sp.nseg] >> 2;
+    unsigned long long m = 0;
+    for (int s = s_first; s <= s_last; ++s) {
+      if (sp.vstart[s + 1] == sp.vstart[s]) continue;  // empty: no CTA owns it
       const uint32_t c0 = cta_of_word(sp.vstart[s] >> 2, tw, gridDim.x);
       const uint32_t c1 = cta_of_word((sp.vstart[s + 1] >> 2) - 1, tw, gridDim.x);
-      last = (atomicAdd(tk.ticket + s, 1u) == c1 - c0) ? 1u : 0u;
+      if (atomicAdd(tk.ticket + s, 1u) == c1 - c0) m |= 1ull << s;
     }
-    __syncthreads();
-    if (last) {
-      __threadfence();
-      for (uint32_t b = threadIdx.x; b < 256; b += blockDim.x) out[b] = atomicExch(dst + b, 0ull);
+    lastmask = m;
+  }
+  __syncthreads();
+  unsigned long long m = lastmask;
+  if (m) {
+    __threadfence();
+    while (m) {
+      const int s = __ffsll(m) - 1;
+      m &= m - 1;
+      for (uint32_t b = threadIdx.x; b < 256; b += blockDim.x)
+        out[size_t(sp.out_base + s) * 256 + b] = atomicExch(tk.acc + size_t(s) * 256 + b, 0ull);
       if (threadIdx.x == 0) tk.ticket[s] = 0;
     }
   }
-  compiler_fence();
-  __syncthreads();
 }
 
 // The streaming loop of one piece, written lean for the 32-register budget of 64
@@ -357,6 +390,7 @@ __global__ void __launch_bounds__(TH, kLaneMinBlocks)
     k_lane(const uint8_t* __restrict__ data, const __grid_constant__ SegParams sp, int hot_bin,
            unsigned long long* __restrict__ out, Tickets tk, const uint32_t* __restrict__ decision) {
   __shared__ __align__(16) uint32_t counters[256 * 32];
+  HS_STAMP(0);
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(counters);
   for (uint32_t i = threadIdx.x; i < kLaneArrayBytes / 16; i += blockDim.x) sh_st4(sbase + i * 16, make_uint4(0, 0, 0, 0));
   __syncthreads();
@@ -378,10 +412,34 @@ __global__ void __launch_bounds__(TH, kLaneMinBlocks)
   // u32 columns: a column adds at most (CTA bytes)/32 <= 2^32, so one flush per
   // (CTA, segment) suffices -- required by the ticketed output
   const uint32_t hot4 = hot * 0x01010101u;
-  for_each_piece<~0ull>(sp, [&](int s, uint64_t p0, uint64_t p1) {
-    lane_piece<U, HOT, TH>(data, p0, p1, tb, hot4);
-    lane_flush(sbase, out + size_t(sp.out_base + s) * 256, tk, sp, s);
-  });
+  // The CTA's pieces (segment, byte range) are listed in shared memory first, so no
+  // segment-walk state is live across the streaming loop (it would take registers the
+  // loop needs at 64 resident warps).
+  __shared__ uint64_t pc_p0[kMaxSeg], pc_p1[kMaxSeg];
+  __shared__ int pc_seg[kMaxSeg];
+  __shared__ int pc_n;
+  if (threadIdx.x == 0) {
+    int n = 0;
+    for_each_piece<~0ull>(sp, [&](int s, uint64_t p0, uint64_t p1) {
+      pc_p0[n] = p0;
+      pc_p1[n] = p1;
+      pc_seg[n] = s;
+      ++n;
+    });
+    pc_n = n;
+  }
+  __syncthreads();
+  const bool ticketed = tk.ticket != nullptr;
+  HS_STAMP(1);
+  for (int i = 0; i < pc_n; ++i) {
+    lane_piece<U, HOT, TH>(data, pc_p0[i], pc_p1[i], tb, hot4);
+    HS_STAMP(2 + 2 * i);
+    const int s = pc_seg[i];
+    lane_flush(sbase, ticketed ? tk.acc + size_t(s) * 256 : out + size_t(sp.out_base + s) * 256);
+    HS_STAMP(3 + 2 * i);
+  }
+  if (ticketed && pc_n > 0) lane_tickets(tk, sp, pc_seg[0], pc_seg[pc_n - 1], out);
+  HS_STAMP(15);
 }
 
 // ================================================================== HS_IMPL_WARP
@@ -1091,3 +1149,15 @@ int hs_generate_device(int kind, uint64_t seed, int value, double mean, double s
 }
 
 }  // extern "C"
+
+#ifdef HS_TRACE
+extern "C" int hs_trace_read(void* host, size_t bytes) {
+  if (bytes > sizeof(hs_trace_buf)) bytes = sizeof(hs_trace_buf);
+  return cudaMemcpyFromSymbol(host, hs_trace_buf, bytes) == cudaSuccess ? 0 : -1;
+}
+extern "C" int hs_trace_clear() {
+  void* p = nullptr;
+  if (cudaGetSymbolAddress(&p, hs_trace_buf) != cudaSuccess) return -1;
+  return cudaMemset(p, 0, sizeof(hs_trace_buf)) == cudaSuccess ? 0 : -1;
+}
+#endif
