@@ -249,7 +249,7 @@ __device__ __forceinline__ uint32_t cta_of_word(uint64_t w, uint64_t tw, uint32_
 // a mid-range flush must not wait for its REDs to reach L2 (that round trip under a
 // saturated memory system was ~6 us per CTA; tools/ab_seg.py), so the fence and the
 // tickets are taken once per CTA at the end (lane_tickets).
-__device__ __noinline__ void lane_flush(uint32_t sbase, unsigned long long* __restrict__ dst) {
+__device__ __forceinline__ void lane_flush(uint32_t sbase, unsigned long long* __restrict__ dst) {
   compiler_fence();
   __syncthreads();
   pdl_wait();  // the previous launch on this stream may still own the workspace / outputs
@@ -275,7 +275,7 @@ __device__ __noinline__ void lane_flush(uint32_t sbase, unsigned long long* __re
 // rows: one fence, then a ticket per segment; the last CTA of a segment takes the row
 // with atomicExch(.., 0) (reading and re-zeroing it), stores the output row and resets
 // the ticket, so workspace and tickets are zero again when the launch ends.
-__device__ __noinline__ void lane_tickets(const Tickets& tk, const SegParams& sp, int s_first, int s_last,
+__device__ __forceinline__ void lane_tickets(const Tickets& tk, const SegParams& sp, int s_first, int s_last,
                                           unsigned long long* __restrict__ out) {
   __shared__ unsigned long long lastmask;
   __threadfence();
@@ -306,7 +306,9 @@ __device__ __noinline__ void lane_tickets(const Tickets& tk, const SegParams& sp
 }
 
 // The streaming loop of one piece, written lean for the 32-register budget of 64
-// resident warps: 32-bit vector counts, a running 16-B pointer, compile-time stride.
+// resident warps: the < U*T-vector remainder is counted first, so nothing but the
+// running 16-B pointer, a countdown and the column base is live across the main
+// double-buffered loop; compile-time stride.
 template <int U, bool HOT, int TH>
 __device__ __forceinline__ uint32_t lane_loop(const uint8_t* __restrict__ data, uint64_t a0, uint64_t a1,
                                               uint32_t tb, uint32_t hot4) {
@@ -326,45 +328,52 @@ __device__ __forceinline__ uint32_t lane_loop(const uint8_t* __restrict__ data, 
     }
     word(v.x); word(v.y); word(v.z); word(v.w);
   };
-  const uint4* __restrict__ q = reinterpret_cast<const uint4*>(data + a0) + tid;
   const uint32_t nv = uint32_t((a1 - a0) >> 4);  // pieces are < 2^36 bytes
-  const uint32_t nfull = nv / (U * T);
+  uint32_t nfull = nv / (U * T);
+  {
+    const uint4* __restrict__ r = reinterpret_cast<const uint4*>(data + a0);
+    for (uint32_t i = nfull * U * T + tid; i < nv; i += T) vec(ldg_stream(r + i));
+  }
+  const uint4* __restrict__ q = reinterpret_cast<const uint4*>(data + a0) + tid;
   uint4 A[U], B[U];
   if (nfull > 0) {
 #pragma unroll
     for (int u = 0; u < U; ++u) A[u] = ldg_stream(q + u * T);
   }
-  for (uint32_t j = 0; j < nfull; j += 2) {
-    const bool more = j + 1 < nfull;
-    if (more) {
+  // invariant at the loop head: A holds batch 0 of the nfull batches left at q
+  while (nfull >= 2) {
 #pragma unroll
-      for (int u = 0; u < U; ++u) B[u] = ldg_stream(q + (U + u) * T);
-    }
+    for (int u = 0; u < U; ++u) B[u] = ldg_stream(q + (U + u) * T);
 #pragma unroll
     for (int u = 0; u < U; ++u) vec(A[u]);
-    if (!more) break;
-    if (j + 2 < nfull) {
+    if (nfull > 2) {
 #pragma unroll
       for (int u = 0; u < U; ++u) A[u] = ldg_stream(q + (2 * U + u) * T);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) vec(B[u]);
     q += 2 * U * T;
+    nfull -= 2;
   }
-  for (uint32_t i = nfull * U * T + tid; i < nv; i += T)
-    vec(ldg_stream(reinterpret_cast<const uint4*>(data + a0) + i));
+  if (nfull == 1) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) vec(A[u]);
+  }
   return hotcnt;
 }
 
-// One piece [p0, p1): unaligned head/tail words, then the 16-B body. Compiled as its
-// own function so the segment walk around it does not take its registers. HOT
-// (ADAPTIVE) tests every vector against the CPU pattern's hot bin and adds the
-// register count of hot bytes to the thread's column at the end.
+// One piece [p0, p1): unaligned head/tail words, then the 16-B body. HOT (ADAPTIVE)
+// tests every vector against the CPU pattern's hot bin and adds the register count of
+// hot bytes to the thread's column at the end.
+// Everything in k_lane is inlined: with no calls there is no ABI stack frame, and
+// ptxas keeps the global-memory descriptor in a uniform register (the noinline form
+// re-moved it with 4 R2UR per load pair). tests/test_native_abi.py checks the SASS of
+// the streaming loop (tools/loopcheck.py): no local-memory traffic, no R2UR.
 // (Tried and rejected: verifying the hot bin on a per-CTA sample and switching between
 // the checked and the plain loop at run time -- both loops in one function exceed the
 // 32-register budget of 64 resident warps and the plain loop spills.)
 template <int U, bool HOT, int TH>
-__device__ __noinline__ uint32_t lane_piece(const uint8_t* __restrict__ data, uint64_t p0, uint64_t p1,
+__device__ __forceinline__ uint32_t lane_piece(const uint8_t* __restrict__ data, uint64_t p0, uint64_t p1,
                                             uint32_t tb, uint32_t hot4) {
   const uint32_t tid = threadIdx.x;
   auto word = [&](uint32_t w) {

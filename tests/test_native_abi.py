@@ -105,3 +105,28 @@ def test_stream_engine_abi_validation():
     assert step(p, N.u64p(b), N.u64p(e), 1, p, 4, 0.45, 1, 0, p, p, p, p, None, 0, None) == N.HS_ERR_WORKSPACE
     e6 = np.full(1, 6, np.uint64)
     assert step(p, N.u64p(b), N.u64p(e6), 1, p, 4, 0.45, 1, 0, p, p, p, p, p, ws_need, None) == N.HS_ERR_ALIGNMENT
+
+
+def test_streaming_loop_sass_is_clean():
+    """The k_lane streaming loops (the hot path) compile without local-memory traffic
+    and without per-iteration R2UR moves: both cost measured throughput before
+    (tools/loopcheck.py)."""
+    import shutil
+    import sys
+
+    import pytest
+
+    if shutil.which("cuobjdump") is None:
+        pytest.skip("cuobjdump not available")
+    sys.path.insert(0, str(HEADER.parents[1] / "tools"))
+    import loopcheck
+
+    loops = loopcheck.report(str(N.library_path()))
+    kernels = {r["kernel"] for r in loops}
+    assert len(kernels) == 2, kernels  # plain (1024 threads) and HOT (768 threads) k_lane
+    main = [r for r in loops if r["atoms"] == 64]
+    assert len(main) == 2 and all(r["ldg"] == 4 for r in main), loops
+    for r in loops:
+        assert r["local"] == 0 and r["r2ur"] == 0, r
+    # per 16 B x 4 vectors x 4 bytes: PRMT + address + ATOMS, plus loads and loop control
+    assert all(r["len"] <= 210 for r in main if "Lb0" in r["kernel"]), main

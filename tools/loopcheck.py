@@ -25,18 +25,23 @@ def functions(path):
         yield cur, body
 
 
-def loops(body):
+def back_edges(body):
     for a, t in body:
         if "BRA" not in t:
             continue
         m = re.search(r"0x([0-9a-f]+)\s*$", t)
-        if not m:
+        if m and int(m.group(1), 16) < a:
+            yield int(m.group(1), 16), a
+
+
+def loops(body, innermost=True):
+    edges = list(back_edges(body))
+    for tgt, a in edges:
+        if innermost and any(tgt <= t2 and a2 < a for t2, a2 in edges if (t2, a2) != (tgt, a)):
             continue
-        tgt = int(m.group(1), 16)
-        if tgt < a:
-            ins = [x[1] for x in body if tgt <= x[0] <= a]
-            if sum("ATOMS" in x for x in ins) >= 16:
-                yield tgt, a, ins
+        ins = [x[1] for x in body if tgt <= x[0] <= a]
+        if sum("ATOMS" in x for x in ins) >= 16:
+            yield tgt, a, ins
 
 
 def report(path):

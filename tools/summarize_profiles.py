@@ -43,7 +43,11 @@ def launches(tag, path, command):
         seq.append((r[ki].split("(")[0].replace("void ", "").replace("<unnamed>::", ""), ns))
     first = [i for i, (n, _) in enumerate(seq) if n.startswith("k_lane")][0]
     agg = collections.OrderedDict()
+    fillers = collections.Counter()
     for n, ns in seq[first:]:
+        if "spin_kernel" in n:  # torch.cuda._sleep: bench.py's queue filler before the roofline pass
+            fillers[n] += 1
+            continue
         agg.setdefault(n, []).append(ns)
     tot = sum(sum(v) for v in agg.values())
     lines = [f"# {tag} ncu launch list (gpu__time_duration.sum, --clock-control none), command:", f"#   {command}",
@@ -51,6 +55,8 @@ def launches(tag, path, command):
              f"{'kernel':40s} {'launches':>8s} {'mean_us':>9s} {'share':>6s}"]
     for n, v in agg.items():
         lines.append(f"{n[:40]:40s} {len(v):8d} {sum(v) / len(v) / 1e3:9.2f} {sum(v) / tot:6.3f}")
+    if fillers:
+        lines.append(f"# excluded from the shares (untimed queue filler of the roofline pass): {dict(fillers)}")
     setup = collections.Counter(n for n, _ in seq[:first])
     lines.append(f"# setup before the first histogram launch (input generation, untimed): {dict(setup)}")
     out = ROOT / "profiles" / f"{tag}_launches_summary.txt"
