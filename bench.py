@@ -238,6 +238,7 @@ def main(argv=None):
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--sustain-seconds", type=float, default=2.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extras", action="store_true")
@@ -280,10 +281,9 @@ def main(argv=None):
     # previous kernel's tail instead of waiting behind it
     side = [torch.cuda.Stream(device=dev) for _ in SIGMAS]
     wss = [torch.zeros(int(L.hs_workspace_bytes(64)), dtype=torch.uint8, device=dev) for _ in SIGMAS]
-    launch_events: list[tuple] = []
     dist_on = _dist_on()
 
-    def launch(j, record=False):
+    def launch(j):
         # lag-1 pattern for stream j: its previous step's per-chunk histograms, read back
         # asynchronously while the other streams' kernels ran
         if j in pending:
@@ -293,17 +293,10 @@ def main(argv=None):
             patterns[j] = hs.compute_binning_pattern(hs.Histogram256(prior))
         p = patterns[j]
         sj = side[j]
-        if record:
-            e0 = torch.cuda.Event(enable_timing=True)
-            e0.record(sj)
         st = L.hs_histogram_batched(streams[j].data_ptr(), N.u64p(begin), N.u64p(end), 64, N.HS_KIND_ADAPTIVE,
                                     N.HS_IMPL_AUTO, N.i64p(p.offset), N.i64p(p.count), 960, 8,
                                     outs[j].data_ptr(), wss[j].data_ptr(), wss[j].numel(), sj.cuda_stream)
         N.check(st, "hs_histogram_batched")
-        if record:
-            e1 = torch.cuda.Event(enable_timing=True)
-            e1.record(sj)
-            launch_events.append((e0, e1))
         hb = host[j][flip[j]]
         flip[j] ^= 1
         with torch.cuda.stream(sj):
@@ -312,9 +305,9 @@ def main(argv=None):
         ev.record(sj)
         pending[j] = (ev, hb)
 
-    def step(record=False):
+    def step():
         for j in range(len(SIGMAS)):
-            launch(j, record)
+            launch(j)
         if dist_on:
             # one NCCL all_reduce of the step's 256 counts (2 KiB) joins the shards
             for sj in side:
@@ -368,7 +361,7 @@ def main(argv=None):
         for sj in side:
             sj.wait_stream(stream)
         for _ in range(args.steps):
-            step(record=True)
+            step()
         for sj in side:
             stream.wait_stream(sj)
         t1.record(stream)
@@ -387,6 +380,31 @@ def main(argv=None):
     if dist_on:
         assert int(total_counts.sum().item()) == world * len(SIGMAS) * GiB, "allreduced total"
 
+    # ---- sustained: the same step for ~2 s. This kernel draws ~1000 W at full clocks,
+    # the board's power limit, so after ~50 ms the power controller lowers the SM clock
+    # and the atomic pipe with it (tools/ramp_probe.py). Reported beside
+    # the headline, not instead of it.
+    sustained = None
+    if args.sustain_seconds > 0:
+        n_sus = max(1, int(args.sustain_seconds * 1e3 / (elapsed_ms / args.steps)))
+        barrier(world)
+        torch.cuda.synchronize()
+        s0e, s1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(local) as sus_clocks:
+            s0e.record(stream)
+            for sj in side:
+                sj.wait_stream(stream)
+            for _ in range(n_sus):
+                step()
+            for sj in side:
+                stream.wait_stream(sj)
+            s1e.record(stream)
+            torch.cuda.synchronize()
+        sus_ms = max_over_ranks(s0e.elapsed_time(s1e), world)
+        sustained = {"steps": n_sus, "seconds": round(sus_ms / 1e3, 3),
+                     "value": round(world * bytes_per_step_rank * n_sus / (sus_ms / 1e3) / 1e9, 2), "unit": "GB/s",
+                     "clocks": sus_clocks.summary()}
+
     # ---- roofline of the dominant kernel (k_lane<HOT>, one launch = 1 GiB, 64 segments)
     peak, peak_src = peaks()
     achieved = GiB / (avg_launch_ms / 1e3) / 1e9
@@ -401,7 +419,7 @@ def main(argv=None):
                 "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
                 "achieved_method": "1 GiB / mean launch duration (CUDA events around 10 back-to-back launches per sigma stream, after warm-up, before the timed region)",
                 "concurrent_streams_gbs": round(value / world, 1),
-                "kernel": "k_lane, kind ADAPTIVE (hs_histogram_batched, 64 x 16 MiB segments; per-launch events on its stream)",
+                "kernel": "k_lane, kind ADAPTIVE (hs_histogram_batched, 64 x 16 MiB segments)",
                 "algorithmic_bytes_per_launch": GiB}
 
     # ---- e2e through the public streaming API with pinned host buffers (rank 0 sizes it)
@@ -433,6 +451,7 @@ def main(argv=None):
             "gpu_launches": len(SIGMAS) * args.steps,  # k_lane launches in the timed region
             "clocks": clocks.summary(),
             "per_launch_ms": {"mean": round(avg_launch_ms, 4), "back_to_back_launches": reps * len(SIGMAS), **per_sigma},
+            "sustained": sustained,
             **extra,
         }
         print(json.dumps(line), flush=True)
