@@ -425,7 +425,7 @@ def main(argv=None):
     # ---- e2e through the public streaming API with pinned host buffers (rank 0 sizes it)
     e2e = None
     if not args.no_e2e:
-        e2e = e2e_run(hs, D, torch, streams, world, args.e2e_steps)
+        e2e = e2e_run(hs, D, torch, rank, world, args.e2e_steps)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -573,20 +573,34 @@ def c3_switch(hs, torch, dev):
             "kernel_log": [k.value for k in log], "degeneracy_log": [round(d, 4) for d in rep.degeneracy_log]}
 
 
-def e2e_run(hs, D, torch, streams, world, steps):
-    """The same 3-stream workload through hs.run_pipeline with every chunk in pinned
-    host memory: per iteration the producer H2D-copies a batch of 8 chunks on the copy
-    stream while the consumer's launch for the previous batch runs."""
-    chunks = []
-    for buf in streams:
-        pinned = D.pinned_bytes(GiB)
-        pinned[:] = buf.cpu().numpy()  # setup: one D2H of the generated stream (untimed)
-        words = pinned.view(np.uint32)
-        chunks.extend(hs.PackedChunk(words[c * (CHUNK // 4):(c + 1) * (CHUNK // 4)]) for c in range(64))
+C4_CHUNKS = 1024  # BASELINE configs[3]: 16 GiB host-streamed, 16 MiB chunks
+C4_SEGMENTS = (("uniform", {}), ("normal", {"mean": MEAN, "sigma": 32.0}), ("constant", {"value": 127}),
+               ("normal", {"mean": MEAN, "sigma": 8.0}))
+
+
+def e2e_run(hs, D, torch, rank, world, steps):
+    """BASELINE configs[3] through the public streaming API: a 16 GiB mixed-distribution
+    stream (uniform -> normal sigma 32 -> constant 127 -> normal sigma 8, 256 chunks of
+    16 MiB each, chunk seeds base ^ index as schedule_stream) in pinned host memory,
+    run_pipeline with the reference's switch policy (threshold 0.45, window 8): the
+    producer H2D-copies a batch of 8 chunks on the copy stream while the consumer's
+    launch for the previous batch runs. Ranks take contiguous chunk ranges (replicas of
+    the host path, each over its own link). Wall time of the whole run_pipeline call."""
+    lo, hi = rank * C4_CHUNKS // world, (rank + 1) * C4_CHUNKS // world
+    per_seg = C4_CHUNKS // len(C4_SEGMENTS)
+    pinned = D.pinned_bytes((hi - lo) * CHUNK)  # setup (untimed): page-locking 16 GiB takes ~11 s
+    words = pinned.view(np.uint32)
+    stage = torch.empty(CHUNK, dtype=torch.uint8, device="cuda")
+    for i in range(lo, hi):
+        kind, kw = C4_SEGMENTS[i // per_seg]
+        spec = hs.SourceSpec(kind, CHUNK, (BASE_SEED ^ 0xC4) ^ i, **kw)
+        hs.generate_device(spec, stage)
+        torch.from_numpy(pinned[(i - lo) * CHUNK:(i - lo + 1) * CHUNK]).copy_(stage)
+    chunks = [hs.PackedChunk(words[c * (CHUNK // 4):(c + 1) * (CHUNK // 4)]) for c in range(hi - lo)]
     batch = 8
     iters = len(chunks) // batch
-    cfg = hs.PipelineConfig(num_iterations=iters, chunk_pixels=CHUNK, batch_size=batch, window_size=64)
-    policy = hs.SwitchPolicy(1e-9)  # AHist for every batch, pattern from the window (lag 1)
+    cfg = hs.PipelineConfig(num_iterations=iters, chunk_pixels=CHUNK, batch_size=batch, window_size=8)
+    policy = hs.SwitchPolicy()
 
     def src():
         for i in range(iters):
@@ -602,10 +616,12 @@ def e2e_run(hs, D, torch, streams, world, steps):
         times.append(time.perf_counter() - t0)
         assert acc.running.total() == len(chunks) * CHUNK
     dt = max_over_ranks(float(np.median(times)), world)
+    kinds = [k.value for k in log]
+    switches = sum(1 for a, b in zip(kinds, kinds[1:]) if a != b)
     # copy-only link bandwidth of the same pinned buffer, for the fraction
     dst = torch.empty(GiB, dtype=torch.uint8, device="cuda")
     h2d = []
-    big = torch.from_numpy(D.pinned_bytes(GiB))
+    big = torch.from_numpy(pinned[:GiB])
     for _ in range(3):
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
@@ -619,6 +635,9 @@ def e2e_run(hs, D, torch, streams, world, steps):
     link = max(h2d)
     return {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": total_bytes,
             "d2h_bytes_per_step": len(chunks) * 2048, "api": "paper_1011_0235_b200.run_pipeline (pinned host chunks)",
+            "workload": "C4: 16 GiB mixed stream (uniform/normal32/const127/normal8, 16 MiB chunks, batch 8), "
+                        "reference switch policy", "kernel_switches": switches,
+            "adaptive_iterations": kinds.count("adaptive"), "iterations": len(kinds),
             "h2d_link_gbs": round(link, 2), "frac_of_link": round(value / world / link, 4)}
 
 

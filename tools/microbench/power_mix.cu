@@ -45,11 +45,21 @@ __global__ void __launch_bounds__(1024, 2) k_hist(const uint4* in, size_t nvec, 
   }
 }
 
+__global__ void fill_random(uint64_t* p, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    uint64_t z = (i + 1) * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull; z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    p[i] = z ^ (z >> 31);
+  }
+}
+
 int main(int argc, char** argv) {
   const double secs = argc > 1 ? atof(argv[1]) : 5.0;
   size_t n = (size_t)1 << 30;
   uint8_t* d; cudaMalloc(&d, n);
-  cudaMemset(d, 0x5a, n);
+  if (argc > 2 && argv[2][0] == 'r') fill_random<<<1184, 256>>>((uint64_t*)d, n / 8);
+  else cudaMemset(d, 0x5a, n);
+  cudaDeviceSynchronize();
   unsigned long long* out; cudaMalloc(&out, 4096);
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
