@@ -271,12 +271,19 @@ def main(argv=None):
     torch.cuda.synchronize()
     begin = np.arange(64, dtype=np.uint64) * CHUNK
     end = begin + CHUNK
-    outs = [torch.empty((64, 256), dtype=torch.int64, device=dev) for _ in SIGMAS]
+    # per-chunk outputs double-buffered by step parity, so step k+1's kernels never wait
+    # for step k's allreduce (which reads step k's buffers on its own stream)
+    outs_all = torch.empty((2, len(SIGMAS), 64, 256), dtype=torch.int64, device=dev)
+    outs = [[outs_all[k, j] for k in range(2)] for j in range(len(SIGMAS))]
     host = [[torch.empty((64, 256), dtype=torch.int64, pin_memory=True) for _ in range(2)] for _ in SIGMAS]
     patterns = [hs.uniform_pattern(960) for _ in SIGMAS]
     pending: dict[int, tuple] = {}
     flip = [0, 0, 0]
-    total_counts = torch.zeros(256, dtype=torch.int64, device=dev)
+    total_counts = [torch.zeros(256, dtype=torch.int64, device=dev) for _ in range(2)]
+    red_stream = torch.cuda.Stream(device=dev)
+    red_done = [None, None]
+    host_wait = [0.0]
+    par = [0]
     # one CUDA stream (and workspace) per sigma stream: a kernel's ramp overlaps the
     # previous kernel's tail instead of waiting behind it
     side = [torch.cuda.Stream(device=dev) for _ in SIGMAS]
@@ -288,19 +295,24 @@ def main(argv=None):
         # asynchronously while the other streams' kernels ran
         if j in pending:
             ev, hb = pending.pop(j)
+            w0 = time.perf_counter()
             ev.synchronize()
+            host_wait[0] += time.perf_counter() - w0
             prior = hb.numpy().view(np.uint64).sum(axis=0, dtype=np.uint64)
             patterns[j] = hs.compute_binning_pattern(hs.Histogram256(prior))
         p = patterns[j]
         sj = side[j]
+        o = outs[j][par[0]]
+        if red_done[par[0]] is not None:
+            sj.wait_event(red_done[par[0]])  # the allreduce two steps back has read o
         st = L.hs_histogram_batched(streams[j].data_ptr(), N.u64p(begin), N.u64p(end), 64, N.HS_KIND_ADAPTIVE,
                                     N.HS_IMPL_AUTO, N.i64p(p.offset), N.i64p(p.count), 960, 8,
-                                    outs[j].data_ptr(), wss[j].data_ptr(), wss[j].numel(), sj.cuda_stream)
+                                    o.data_ptr(), wss[j].data_ptr(), wss[j].numel(), sj.cuda_stream)
         N.check(st, "hs_histogram_batched")
         hb = host[j][flip[j]]
         flip[j] ^= 1
         with torch.cuda.stream(sj):
-            hb.copy_(outs[j], non_blocking=True)
+            hb.copy_(o, non_blocking=True)
         ev = torch.cuda.Event()
         ev.record(sj)
         pending[j] = (ev, hb)
@@ -309,13 +321,18 @@ def main(argv=None):
         for j in range(len(SIGMAS)):
             launch(j)
         if dist_on:
-            # one NCCL all_reduce of the step's 256 counts (2 KiB) joins the shards
+            # one NCCL all_reduce of the step's 256 counts (2 KiB) joins the shards; on its
+            # own stream, overlapped with the next step's kernels
+            k = par[0]
             for sj in side:
-                stream.wait_stream(sj)
-            torch.sum(torch.stack([o.sum(dim=0) for o in outs]), dim=0, out=total_counts)
-            torch.distributed.all_reduce(total_counts)
-            for sj in side:
-                sj.wait_stream(stream)
+                red_stream.wait_stream(sj)
+            with torch.cuda.stream(red_stream):
+                torch.sum(outs_all[k], dim=(0, 1), out=total_counts[k])
+                torch.distributed.all_reduce(total_counts[k])
+                ev = torch.cuda.Event()
+                ev.record(red_stream)
+                red_done[k] = ev
+        par[0] ^= 1
 
     def serial_roofline():
         # ---- roofline: the same launches (same patterns), back to back on one stream, all
@@ -336,7 +353,7 @@ def main(argv=None):
             for _ in range(reps):
                 N.check(L.hs_histogram_batched(streams[j].data_ptr(), N.u64p(begin), N.u64p(end), 64, N.HS_KIND_ADAPTIVE,
                                                N.HS_IMPL_AUTO, N.i64p(p.offset), N.i64p(p.count), 960, 8,
-                                               outs[j].data_ptr(), wss[0].data_ptr(), wss[0].numel(), s0.cuda_stream),
+                                               outs[j][0].data_ptr(), wss[0].data_ptr(), wss[0].numel(), s0.cuda_stream),
                         "hs_histogram_batched")
             b.record(s0)
             ev.append((j, a, b))
@@ -360,10 +377,15 @@ def main(argv=None):
         t0.record(stream)
         for sj in side:
             sj.wait_stream(stream)
+        h0 = time.perf_counter()
+        host_wait[0] = 0.0
         for _ in range(args.steps):
             step()
+        host_issue_ms = (time.perf_counter() - h0) * 1e3 / args.steps
+        host_wait_ms = host_wait[0] * 1e3 / args.steps
         for sj in side:
             stream.wait_stream(sj)
+        stream.wait_stream(red_stream)
         t1.record(stream)
         torch.cuda.synchronize()
     barrier(world)
@@ -375,10 +397,10 @@ def main(argv=None):
 
     # ---- correctness spot check of the last step against closed-form totals
     for j in range(len(SIGMAS)):
-        got = outs[j].sum().item()
+        got = outs[j][par[0] ^ 1].sum().item()
         assert got == GiB, f"stream {j}: counted {got} != {GiB}"
     if dist_on:
-        assert int(total_counts.sum().item()) == world * len(SIGMAS) * GiB, "allreduced total"
+        assert int(total_counts[par[0] ^ 1].sum().item()) == world * len(SIGMAS) * GiB, "allreduced total"
 
     # ---- sustained: the same step for ~2 s. This kernel draws ~1000 W at full clocks,
     # the board's power limit, so after ~50 ms the power controller lowers the SM clock
@@ -398,6 +420,7 @@ def main(argv=None):
                 step()
             for sj in side:
                 stream.wait_stream(sj)
+            stream.wait_stream(red_stream)
             s1e.record(stream)
             torch.cuda.synchronize()
         sus_ms = max_over_ranks(s0e.elapsed_time(s1e), world)
@@ -452,6 +475,8 @@ def main(argv=None):
             "clocks": clocks.summary(),
             "per_launch_ms": {"mean": round(avg_launch_ms, 4), "back_to_back_launches": reps * len(SIGMAS), **per_sigma},
             "sustained": sustained,
+            "host_issue_ms_per_step": round(host_issue_ms, 4),
+            "host_wait_ms_per_step": round(host_wait_ms, 4),
             **extra,
         }
         print(json.dumps(line), flush=True)
