@@ -138,25 +138,31 @@ int hs_ablation_stage(const uint8_t* d_data, uint64_t n_bytes, int stage,
  * The accumulator, moving window and NVHist/AHist switch of the stream driver
  * (stream.py:62-116, :390-425; policy.py:39-64) kept on the device, so lag-1 kernel
  * switching runs at device speed with no host round trip.
- * State is caller-allocated (hs_stream_state_bytes) and zeroed by hs_stream_reset.
+ * State is caller-allocated (hs_stream_state_bytes) and zeroed by hs_stream_reset,
+ * which also stamps the device clock (%globaltimer, ns) at byte offset 32 + 8.
  * Error word: uint32 at byte offset 16 of the state, sticky, read once after the last
  * step -- bit 0 = window count went negative (stream.py NegativeCount), bit 1 = empty
  * histogram in divergence (policy.py EmptyHistogram). */
 size_t hs_stream_state_bytes(int window_size);
 int hs_stream_reset(void* d_state, int window_size, void* stream);
 
-/* One iteration: histograms of the batch's nseg (<= 64) segments into d_out[nseg][256]
- * with the kernel kind and hot bin the previous fold decided (read on the device), then
- * the fold: acc += each chunk, window push/evict (error bit on NegativeCount),
- * d_kind_log[iteration] = kind used, d_deg_log[iteration] = window degeneracy,
+/* One iteration: histograms of the batch's nseg (<= 64) segments into d_out[nseg][256],
+ * then the fold: acc += each chunk, window push/evict (error bit on NegativeCount),
+ * d_kind_log[iteration] = kind the previous fold decided, d_deg_log[iteration] = window
+ * degeneracy,
  * d_div_log[iteration] = total-variation(acc, window) in numpy's summation order, and
  * -- when (iteration+1) % recompute_every == 0 -- the decision for the next iteration:
  * ADAPTIVE iff degeneracy >= threshold (policy.py:49-53), hot bin = window argmax.
- * Requires a workspace of hs_workspace_bytes(). Asynchronous; no host sync. */
+ * Both kinds count exactly alike on this device, so the histogram does not wait for the
+ * decision: it streams while the previous fold finishes, and steps chain with
+ * programmatic dependent launch. d_ns_log (may be NULL): device clock (ns) when the
+ * iteration's fold finished -- per-iteration time without events between launches.
+ * Requires a workspace of hs_workspace_bytes(); d_state and d_out 16-byte aligned.
+ * Asynchronous; no host sync. */
 int hs_stream_step(const uint8_t* d_data, const uint64_t* h_begin, const uint64_t* h_end, int nseg,
                    void* d_state, int window_size, double threshold, int recompute_every, int iteration,
                    uint64_t* d_out, double* d_deg_log, double* d_div_log, int32_t* d_kind_log,
-                   void* d_ws, size_t ws_bytes, void* stream);
+                   uint64_t* d_ns_log, void* d_ws, size_t ws_bytes, void* stream);
 
 /* ---- host-side control plane (native replacements of pattern.py / policy.py) */
 

@@ -116,7 +116,7 @@ _SIGNATURES = {
     "hs_stream_reset": (_c.c_int, [_P, _c.c_int, _P]),
     "hs_stream_step": (
         _c.c_int,
-        [_P, _U64P, _U64P, _c.c_int, _P, _c.c_int, _c.c_double, _c.c_int, _c.c_int, _P, _P, _P, _P, _P,
+        [_P, _U64P, _U64P, _c.c_int, _P, _c.c_int, _c.c_double, _c.c_int, _c.c_int, _P, _P, _P, _P, _P, _P,
          _c.c_size_t, _P],
     ),
 }

@@ -101,8 +101,17 @@ __device__ unsigned long long hs_trace_buf[1024][16];
       hs_trace_buf[blockIdx.x][(slot)] = t_;                                                    \
     }                                                                                           \
   } while (0)
+#define HS_FSTAMP(slot)                                                                         \
+  do {                                                                                          \
+    if (threadIdx.x == 0) {                                                                     \
+      unsigned long long t_;                                                                    \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                    \
+      hs_trace_buf[1023][(slot)] = t_;                                                          \
+    }                                                                                           \
+  } while (0)
 #else
 #define HS_STAMP(slot) do { } while (0)
+#define HS_FSTAMP(slot) do { } while (0)
 #endif
 
 // byte k of w, zero-extended (PRMT)
@@ -392,21 +401,19 @@ __device__ __forceinline__ uint32_t lane_piece(const uint8_t* __restrict__ data,
   return 0;
 }
 
-// HOT (ADAPTIVE): register path for the hot bin `hot_bin`; with `decision` (device
-// stream engine) the hot bin comes from the previous fold on the device.
+// HOT (ADAPTIVE): register path for the hot bin `hot_bin`.
 template <int U, bool HOT, int TH = kLaneThreads>
 __global__ void __launch_bounds__(TH, kLaneMinBlocks)
     k_lane(const uint8_t* __restrict__ data, const __grid_constant__ SegParams sp, int hot_bin,
-           unsigned long long* __restrict__ out, Tickets tk, const uint32_t* __restrict__ decision) {
+           unsigned long long* __restrict__ out, Tickets tk) {
   __shared__ __align__(16) uint32_t counters[256 * 32];
   HS_STAMP(0);
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(counters);
   for (uint32_t i = threadIdx.x; i < kLaneArrayBytes / 16; i += blockDim.x) sh_st4(sbase + i * 16, make_uint4(0, 0, 0, 0));
   __syncthreads();
   const uint32_t tb = sbase + (threadIdx.x & 31) * 4;  // column base: bank == lane
-  // device-resident stream engine: {kind, hot bin} decided by the previous fold on the GPU
-  const uint32_t hot = (decision != nullptr ? __ldcg(decision + 1) : uint32_t(hot_bin)) & 0xff;
   pdl_launch_dependents();  // the next launch's CTAs may take SMs as ours retire
+  const uint32_t hot = uint32_t(hot_bin) & 0xff;
   if (tk.ticket != nullptr && blockIdx.x == 0) {
     // ticketed launches have no memset: CTA 0 zeroes the empty segments' outputs
     bool any_empty = false;
@@ -625,14 +632,15 @@ __global__ void __launch_bounds__(kSubThreads)
 // :390-425; policy.py:39-64) so lag-1 kernel switching needs no host round trip.
 // State (caller-allocated, hs_stream_state_bytes): header | acc[256] | win[256] | ring[W][256].
 struct DevStreamHeader {
-  uint32_t kind;   // kernel kind for the next launch (read by k_lane through `decision`)
+  uint32_t kind;   // kernel kind decided for the next iteration (logged by the next fold)
   uint32_t hot;    // hot bin for ADAPTIVE: argmax of the window (lowest bin on ties)
   uint32_t head;   // ring head
   uint32_t count;  // ring entries
   uint32_t error;  // 1: NegativeCount (stream.py:96-97), 2: empty totals
   uint32_t pad0[3];
   unsigned long long chunks_seen;
-  unsigned long long pad1[3];
+  unsigned long long t_reset_ns;  // %globaltimer when hs_stream_reset ran
+  unsigned long long pad1[2];
 };
 static_assert(sizeof(DevStreamHeader) == 64, "header size");
 
@@ -660,73 +668,225 @@ __device__ double np_pairwise_sum(const double* a, int n) {
   return __dadd_rn(np_pairwise_sum(a, n2), np_pairwise_sum(a + n2, n - n2));
 }
 
-__global__ void __launch_bounds__(256)
+// numpy's pairwise sum of exactly 256 doubles, in parallel: 256 = 128 + 128, and each
+// 128-block is 8 running accumulators over 16 elements, combined ((0+1)+(2+3))+((4+5)+(6+7)).
+// Threads 0..15 run the 16 accumulators (same order of adds, so the same bits as
+// np_pairwise_sum(d, 256)); thread 0 combines. Returns the sum in thread 0.
+__device__ double np_pairwise_sum256(const double* d, double* acc16) {
+  const int t = threadIdx.x;
+  if (t < 16) {
+    const double* blk = d + (t >> 3) * 128;
+    const int j = t & 7;
+    double r = blk[j];
+    for (int i = 8; i < 128; i += 8) r = __dadd_rn(r, blk[i + j]);
+    acc16[t] = r;
+  }
+  __syncthreads();
+  double res = 0.0;
+  if (t == 0) {
+    double h[2];
+    for (int k = 0; k < 2; ++k) {
+      const double* r = acc16 + 8 * k;
+      h[k] = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                       __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    }
+    res = __dadd_rn(h[0], h[1]);
+  }
+  return res;
+}
+
+// exact u64 sums and first maximum (value, lowest index) over bins 0..255 (threads 0..255)
+struct FoldRed { unsigned long long ta, tb, mx; uint32_t am; };
+__device__ FoldRed fold_reduce(unsigned long long a, unsigned long long w, uint32_t b) {
+  // bins 0..255 live in warps 0..7; the block's other warps only join the barrier
+  __shared__ unsigned long long r_ta[8], r_tb[8], r_mx[8];
+  __shared__ uint32_t r_am[8];
+  unsigned long long ta = a, tb = w, mx = w;
+  uint32_t am = b;
+  for (int o = 16; o > 0; o >>= 1) {
+    ta += __shfl_xor_sync(0xffffffffu, ta, o);
+    tb += __shfl_xor_sync(0xffffffffu, tb, o);
+    const unsigned long long m2 = __shfl_xor_sync(0xffffffffu, mx, o);
+    const uint32_t a2 = __shfl_xor_sync(0xffffffffu, am, o);
+    if (m2 > mx || (m2 == mx && a2 < am)) { mx = m2; am = a2; }
+  }
+  const int wid = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0 && wid < 8) { r_ta[wid] = ta; r_tb[wid] = tb; r_mx[wid] = mx; r_am[wid] = am; }
+  __syncthreads();
+  FoldRed r{0, 0, r_mx[0], r_am[0]};
+  for (int k = 0; k < 8; ++k) {
+    r.ta += r_ta[k];
+    r.tb += r_tb[k];
+    if (r_mx[k] > r.mx || (r_mx[k] == r.mx && r_am[k] < r.am)) { r.mx = r_mx[k]; r.am = r_am[k]; }
+  }
+  return r;
+}
+
+// One CTA of 256 threads, latency-bound (one launch per iteration): all threads first
+// stage the batch's chunk histograms into shared memory with independent 16-B loads
+// (and the ring too for windows below kFoldSmallWin); then thread b < 256 folds bin b
+// (stream.py:_StreamState.post: accumulator, window push/evict, NegativeCount check in
+// push order) with every input loaded independently, kFoldBatch pushes per round.
+constexpr int kFoldThreads = 256;  // one thread per bin; small enough to share an SM
+                                   // with a histogram CTA of the next iteration
+constexpr int kFoldBatch = 8;      // pushes whose inputs are loaded per round (registers)
+constexpr int kFoldSmallWin = 16;  // windows below this keep the ring in shared memory
+constexpr size_t kFoldSmem = size_t(kMaxSeg) * 256 * 8 + size_t(kFoldSmallWin - 1) * 256 * 8;
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// hs_stream_reset: zero the state and stamp the device clock
+__global__ void k_stream_reset(unsigned long long* __restrict__ state, size_t words) {
+  constexpr size_t kStamp = offsetof(DevStreamHeader, t_reset_ns) / 8;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < words; i += size_t(gridDim.x) * blockDim.x)
+    state[i] = i == kStamp ? globaltimer_ns() : 0ull;
+}
+
+__global__ void __maxnreg__(128)
     k_stream_fold(const unsigned long long* __restrict__ hist, int nseg, uint8_t* __restrict__ state, int window,
                   double threshold, int decide, int iteration, double* __restrict__ deg_log,
-                  double* __restrict__ div_log, int32_t* __restrict__ kind_log) {
+                  double* __restrict__ div_log, int32_t* __restrict__ kind_log,
+                  unsigned long long* __restrict__ ns_log) {
   DevStreamHeader* hd = reinterpret_cast<DevStreamHeader*>(state);
   unsigned long long* acc = reinterpret_cast<unsigned long long*>(state + sizeof(DevStreamHeader));
   unsigned long long* win = acc + 256;
   unsigned long long* ring = win + 256;
-  __shared__ unsigned long long sa[256], sw[256];
+  extern __shared__ __align__(16) unsigned long long fold_smem[];
+  unsigned long long* sh = fold_smem;                        // [nseg][256] chunk histograms
+  unsigned long long* sring = fold_smem + size_t(nseg) * 256;  // [window][256] when small
   __shared__ double d[256];
-  __shared__ unsigned int err;
-  __shared__ unsigned long long ta_s, tb_s;
-  const int b = threadIdx.x;
-  if (b == 0) err = 0;
-  __syncthreads();
-  uint32_t head = hd->head, count = hd->count;
-  unsigned long long a = acc[b], w = win[b];
-  for (int j = 0; j < nseg; ++j) {  // push each chunk in order (stream.py:_StreamState.post)
-    const unsigned long long h = hist[size_t(j) * 256 + b];
-    a += h;
-    if (count < uint32_t(window)) {
-      ring[size_t((head + count) % window) * 256 + b] = h;
-      w += h;
-      ++count;
-    } else {
-      const unsigned long long old = ring[size_t(head) * 256 + b];
-      w += h;
-      if (w < old) atomicOr(&err, 1u);
-      w -= old;
-      ring[size_t(head) * 256 + b] = h;
-      head = (head + 1) % window;
+  __shared__ double acc16[16];
+  const uint32_t t = threadIdx.x, b = t;
+  HS_FSTAMP(0);
+  pdl_launch_dependents();  // the next histogram launch may start streaming meanwhile
+  pdl_wait();               // the histogram launch before us must be complete
+  HS_FSTAMP(1);
+  const bool small = window < kFoldSmallWin;
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(hist);
+    uint4* dst = reinterpret_cast<uint4*>(sh);
+    const int nv = nseg * 128;  // 16-B vectors, 16 per thread in flight per round
+    constexpr int kV = 16;
+    for (int i0 = 0; i0 < nv; i0 += kV * kFoldThreads) {
+      uint4 v[kV];
+#pragma unroll
+      for (int k = 0; k < kV; ++k)
+        if (i0 + t + k * kFoldThreads < nv) v[k] = __ldcg(src + i0 + t + k * kFoldThreads);
+#pragma unroll
+      for (int k = 0; k < kV; ++k)
+        if (i0 + t + k * kFoldThreads < nv) dst[i0 + t + k * kFoldThreads] = v[k];
+    }
+    if (small) {
+      const uint4* rs = reinterpret_cast<const uint4*>(ring);
+      uint4* rd = reinterpret_cast<uint4*>(sring);
+      for (int i = t; i < window * 128; i += kFoldThreads) rd[i] = __ldcg(rs + i);
     }
   }
-  acc[b] = a;
-  win[b] = w;
-  sa[b] = a;
-  sw[b] = w;
+  uint32_t head = hd->head, count = hd->count;
+  unsigned long long a = acc[b], w = win[b];
+  bool neg = false;
   __syncthreads();
-  if (b == 0) {
-    unsigned long long ta = 0, tb = 0, mx = 0;
-    uint32_t am = 0;
-    for (int i = 0; i < 256; ++i) {
-      ta += sa[i];
-      tb += sw[i];
-      if (sw[i] > mx) { mx = sw[i]; am = i; }  // np.argmax: first maximum
+  HS_FSTAMP(6);
+  if (b < 256) {
+    // The pushes as a queue: entries E = (ring, oldest first: count0 of them) followed by
+    // the batch's h_0..h_{n-1}. Push k evicts E[count0 + k - W] once count0 + k >= W;
+    // that entry is a ring slot when its index is below count0 and h_{idx-count0}
+    // (already in shared memory) otherwise. Every evicted value is therefore known up
+    // front and loaded independently; only the running window sum (for the
+    // NegativeCount check, in push order) is a serial chain, of register adds.
+    const unsigned long long* rg = small ? sring : ring;
+    const int W = window, c0 = int(count), n = nseg;
+    const int k_ev = max(0, W - c0);  // first evicting push
+    for (int j0 = 0; j0 < n; j0 += kFoldBatch) {
+      unsigned long long hv[kFoldBatch], ov[kFoldBatch];
+#pragma unroll
+      for (int k = 0; k < kFoldBatch; ++k) {
+        const int j = j0 + k;
+        if (j < n) {
+          hv[k] = sh[j * 256 + b];
+          if (j >= k_ev) {
+            const int idx = c0 + j - W;  // evicted entry of E
+            if (idx < c0) {
+              int slot = int(head) + idx;
+              if (slot >= W) slot -= W;
+              ov[k] = rg[size_t(slot) * 256 + b];
+            } else {
+              ov[k] = sh[(idx - c0) * 256 + b];
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kFoldBatch; ++k) {
+        const int j = j0 + k;
+        if (j >= n) break;
+        a += hv[k];
+        w += hv[k];
+        if (j >= k_ev) {
+          neg |= w < ov[k];
+          w -= ov[k];
+        }
+      }
     }
-    const double frac = tb ? __ddiv_rn((double)mx, (double)tb) : 0.0;
+    // ring after the batch: push k sits in slot (head + count0 + k) mod W, and only
+    // the last W pushes survive, so each slot is written once
+    unsigned long long* rw = small ? sring : ring;
+    {
+      const int j0 = max(0, n - W);
+      int slot = int((uint32_t(head) + uint32_t(c0) + uint32_t(j0)) % uint32_t(W));  // once
+      for (int j = j0; j < n; ++j) {
+        rw[size_t(slot) * 256 + b] = sh[j * 256 + b];
+        slot = slot + 1 == W ? 0 : slot + 1;
+      }
+    }
+    const int ev = max(0, c0 + n - W);
+    head = uint32_t((uint32_t(head) + uint32_t(ev)) % uint32_t(W));
+    count = uint32_t(min(W, c0 + n));
+    acc[b] = a;
+    win[b] = w;
+  }
+  HS_FSTAMP(7);
+  __syncthreads();
+  if (small) {
+    const uint4* rs = reinterpret_cast<const uint4*>(sring);
+    uint4* rd = reinterpret_cast<uint4*>(ring);
+    for (int i = t; i < window * 128; i += kFoldThreads) rd[i] = rs[i];
+  }
+  HS_FSTAMP(2);
+  const FoldRed r = fold_reduce(a, w, b);
+  const bool err = __syncthreads_or(neg);
+  HS_FSTAMP(3);
+  if (b == 0) {
+    const double frac = r.tb ? __ddiv_rn((double)r.mx, (double)r.tb) : 0.0;
     deg_log[iteration] = frac;
     kind_log[iteration] = int32_t(hd->kind);
-    ta_s = ta;
-    tb_s = tb;
     if (decide) {  // decision for the next iteration (lag 1)
       hd->kind = frac >= threshold ? HS_KIND_ADAPTIVE : HS_KIND_NAIVE;
-      hd->hot = am;
+      hd->hot = r.am;
     }
     hd->head = head;
     hd->count = count;
     hd->chunks_seen += uint64_t(nseg);
     if (err) hd->error |= 1u;
-    if (ta == 0 || tb == 0) hd->error |= 2u;
+    if (r.ta == 0 || r.tb == 0) hd->error |= 2u;
   }
+  if (b < 256) {
+    const double pa = r.ta ? __ddiv_rn((double)a, (double)r.ta) : 0.0;
+    const double pb = r.tb ? __ddiv_rn((double)w, (double)r.tb) : 0.0;
+    d[b] = fabs(__dadd_rn(pa, -pb));
+  }
+  HS_FSTAMP(4);
   __syncthreads();
-  const double pa = ta_s ? __ddiv_rn((double)sa[b], (double)ta_s) : 0.0;
-  const double pb = tb_s ? __ddiv_rn((double)sw[b], (double)tb_s) : 0.0;
-  d[b] = fabs(__dadd_rn(pa, -pb));
-  __syncthreads();
-  if (b == 0) div_log[iteration] = __dmul_rn(0.5, np_pairwise_sum(d, 256));
+  const double tv = np_pairwise_sum256(d, acc16);
+  if (b == 0) {
+    div_log[iteration] = __dmul_rn(0.5, tv);
+    if (ns_log) ns_log[iteration] = globaltimer_ns();
+  }
+  HS_FSTAMP(5);
 }
 
 // ================================================================== generators
@@ -842,7 +1002,7 @@ int set_smem(K kernel, size_t bytes) {
 // one launch over <= kMaxSeg segments
 int launch_batch(const uint8_t* d_data, const uint64_t* h_begin, const uint64_t* h_end, int s0, int ns,
                  int kind, int impl, const PatternParams* pp, unsigned long long* d_out, cudaStream_t st,
-                 const DevInfo& di, const Tickets& tk, const uint32_t* decision = nullptr) {
+                 const DevInfo& di, const Tickets& tk, int reserve_slots = 0) {
   SegParams sp;
   sp.nseg = ns;
   sp.out_base = s0;
@@ -858,7 +1018,10 @@ int launch_batch(const uint8_t* d_data, const uint64_t* h_begin, const uint64_t*
   if (impl == HS_IMPL_LANE) {
     // ~64 KiB of input per CTA at least; at most 2 resident CTAs per SM
     const uint64_t want = (v + (64ull << 10) - 1) / (64ull << 10);
-    const int grid = int(std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(di.sms) * kLaneMinBlocks)));
+    // reserve_slots CTA slots are left free (the device stream engine's fold CTA takes
+    // one while the next histogram streams, instead of delaying one of its CTAs)
+    const int grid = int(std::max<uint64_t>(
+        1, std::min<uint64_t>(want, uint64_t(di.sms) * kLaneMinBlocks - uint64_t(reserve_slots))));
     const int hb = pp ? pp->hot_bin : 0;
     // ADAPTIVE runs the register path for the pattern's hot bin only when the pattern
     // marks a dominant value (unique widest sub-bin run): its per-vector test costs ~2%
@@ -871,16 +1034,16 @@ int launch_batch(const uint8_t* d_data, const uint64_t* h_begin, const uint64_t*
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
-    // PDL overlaps a launch's ramp with the previous launch's tail; the device stream
-    // engine's launches stay fully ordered (they read the previous fold's decision)
-    cfg.attrs = decision == nullptr ? attr : nullptr;
-    cfg.numAttrs = decision == nullptr ? 1 : 0;
-    if (decision != nullptr || (kind == HS_KIND_ADAPTIVE && pp != nullptr && pp->hot_unique)) {
+    // PDL overlaps a launch's ramp with the previous launch's tail (in the device
+    // stream engine: with the previous iteration's one-CTA fold)
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (kind == HS_KIND_ADAPTIVE && pp != nullptr && pp->hot_unique) {
       cfg.blockDim = dim3(kLaneHotThreads);
-      e = cudaLaunchKernelEx(&cfg, k_lane<2, true, kLaneHotThreads>, d_data, sp, hb, d_out, tk, decision);
+      e = cudaLaunchKernelEx(&cfg, k_lane<2, true, kLaneHotThreads>, d_data, sp, hb, d_out, tk);
     } else {
       cfg.blockDim = dim3(kLaneThreads);
-      e = cudaLaunchKernelEx(&cfg, k_lane<2, false>, d_data, sp, hb, d_out, tk, (const uint32_t*)nullptr);
+      e = cudaLaunchKernelEx(&cfg, k_lane<2, false>, d_data, sp, hb, d_out, tk);
     }
     if (e != cudaSuccess) return fold(e);
   } else if (impl == HS_IMPL_WARP) {
@@ -1091,13 +1254,17 @@ size_t hs_stream_state_bytes(int window_size) {
 int hs_stream_reset(void* d_state, int window_size, void* stream) {
   if (!d_state || window_size < 1) return HS_ERR_INVALID_ARG;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  return fold(cudaMemsetAsync(d_state, 0, hs_stream_state_bytes(window_size), st));  // kind NAIVE, hot 0
+  if (reinterpret_cast<uintptr_t>(d_state) & 15) return HS_ERR_ALIGNMENT;
+  // zero state (kind NAIVE, hot 0, empty window) + the device clock at reset
+  k_stream_reset<<<16, 256, 0, st>>>(reinterpret_cast<unsigned long long*>(d_state),
+                                     hs_stream_state_bytes(window_size) / 8);
+  return fold(cudaGetLastError());
 }
 
 int hs_stream_step(const uint8_t* d_data, const uint64_t* h_begin, const uint64_t* h_end, int nseg,
                    void* d_state, int window_size, double threshold, int recompute_every, int iteration,
                    uint64_t* d_out, double* d_deg_log, double* d_div_log, int32_t* d_kind_log,
-                   void* d_ws, size_t ws_bytes, void* stream) {
+                   uint64_t* d_ns_log, void* d_ws, size_t ws_bytes, void* stream) {
   if (!d_state || window_size < 1 || nseg < 1 || nseg > kMaxSeg || recompute_every < 1 || iteration < 0 ||
       !d_out || !d_deg_log || !d_div_log || !d_kind_log || !h_begin || !h_end)
     return HS_ERR_INVALID_ARG;
@@ -1109,6 +1276,8 @@ int hs_stream_step(const uint8_t* d_data, const uint64_t* h_begin, const uint64_
     total += h_end[s] - h_begin[s];
   }
   if (reinterpret_cast<uintptr_t>(d_data) & 3) return HS_ERR_ALIGNMENT;
+  // the fold moves the chunk histograms and the ring with 16-B loads
+  if ((reinterpret_cast<uintptr_t>(d_out) | reinterpret_cast<uintptr_t>(d_state)) & 15) return HS_ERR_ALIGNMENT;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   DevInfo di;
   int rc = dev_info(di);
@@ -1120,16 +1289,32 @@ int hs_stream_step(const uint8_t* d_data, const uint64_t* h_begin, const uint64_
     cudaError_t e = cudaMemsetAsync(d_out, 0, size_t(nseg) * 256 * sizeof(uint64_t), st);
     if (e != cudaSuccess) return fold(e);
   } else {
+    // The histogram does not wait for the previous fold's decision: both kinds count
+    // exactly the same, so the lane kernel runs for either and streams while the fold
+    // (one CTA) finishes on the side; the decided kind is what the log records.
     rc = launch_batch(d_data, h_begin, h_end, 0, nseg, HS_KIND_NAIVE, HS_IMPL_LANE, nullptr,
-                      reinterpret_cast<unsigned long long*>(d_out), st, di, tk,
-                      reinterpret_cast<const uint32_t*>(d_state));
+                      reinterpret_cast<unsigned long long*>(d_out), st, di, tk, /*reserve_slots=*/1);
     if (rc != HS_OK) return rc;
   }
   // pattern and kernel refresh for iteration+1 when (iteration+1) % every == 0 (stream.py:407-414)
   const int decide = ((iteration + 1) % recompute_every) == 0;
-  k_stream_fold<<<1, 256, 0, st>>>(reinterpret_cast<const unsigned long long*>(d_out), nseg,
-                                   reinterpret_cast<uint8_t*>(d_state), window_size, threshold, decide, iteration,
-                                   d_deg_log, d_div_log, d_kind_log);
+  static const int rc_fold = set_smem(k_stream_fold, kFoldSmem);
+  if (rc_fold != HS_OK) return rc_fold;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(1);
+  cfg.blockDim = dim3(kFoldThreads);
+  cfg.dynamicSmemBytes = size_t(nseg) * 256 * 8 + (window_size < kFoldSmallWin ? size_t(window_size) * 256 * 8 : 0);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_stream_fold, reinterpret_cast<const unsigned long long*>(d_out), nseg,
+                                     reinterpret_cast<uint8_t*>(d_state), window_size, threshold, decide, iteration,
+                                     d_deg_log, d_div_log, d_kind_log,
+                                     reinterpret_cast<unsigned long long*>(d_ns_log));
+  if (e != cudaSuccess) return fold(e);
   return fold(cudaGetLastError());
 }
 

@@ -167,6 +167,15 @@ def stage(chunks: Sequence, staging: Staging | None, stream=None) -> StagedBatch
     pinned) into ``staging``'s buffer at word-aligned offsets on ``stream``; device
     chunks are referenced in place. Records ``ready`` after the copies."""
     t = require_cuda()
+    if chunks and all(type(c) is DeviceChunk for c in chunks):
+        # fast path (device-resident batches, e.g. the device stream engine): addresses
+        # and sizes are cached on the chunks, so staging 64 chunks is a few microseconds
+        ptrs = np.array([c._ptr for c in chunks], dtype=np.uint64)
+        sizes = np.array([c._n for c in chunks], dtype=np.uint64)
+        nz = sizes > 0
+        base = int(ptrs[nz].min()) if nz.any() else 0
+        begin = np.where(nz, ptrs - np.uint64(base), np.uint64(0)).astype(np.uint64)
+        return StagedBatch(base, begin, begin + sizes, [c.data for c in chunks], None)
     stream = stream or t.cuda.current_stream()
     host = [(i, c) for i, c in enumerate(chunks) if isinstance(c, PackedChunk)]
     ptrs = [0] * len(chunks)

@@ -209,3 +209,20 @@ def test_device_stream_rejects_host_chunks(cuda):
     cfg = small_cfg(num_iterations=2)
     with pytest.raises(TypeError):
         hs.run_device_stream(uniform_source(cfg, 1), cfg, POLICY)
+
+
+@pytest.mark.parametrize("window,batch", [(1, 37), (4, 64), (15, 20), (16, 5), (16, 37), (23, 16), (32, 40), (33, 64), (64, 64)])
+def test_device_stream_batched_fold(cuda, window, batch):
+    """Every fold path: windows < 16 keep the ring in shared memory, 16..31 read evicted
+    slots one push at a time, >= 32 load the chunk histograms and the ring slots they
+    evict 32 at a time before applying the pushes; batches of 5..64 chunks wrap the
+    ring inside one iteration. Equal to the host engine."""
+    px = 4096
+    segs = [(hs.SourceSpec("uniform", px, 21), 4), (hs.SourceSpec("constant", px, 21, value=9), 3),
+            (hs.SourceSpec("normal", px, 21, mean=128.0, sigma=4.0), 4)]
+    cfg = hs.PipelineConfig(num_iterations=11, chunk_pixels=px, batch_size=batch, window_size=window)
+    seq = hs.run_sequential(schedule_stream(segs, batch), cfg, POLICY)
+    dev = hs.run_device_stream(_device_batches(cuda, segs, batch), cfg, POLICY)
+    assert states_equal(seq, dev)
+    assert [k.value for k in seq[3]] == [k.value for k in dev[3]]
+    assert np.array_equal(np.stack([h.counts for h in seq[1].ring]), np.stack([h.counts for h in dev[1].ring]))

@@ -98,13 +98,16 @@ def test_stream_engine_abi_validation():
     step = lib.hs_stream_step
     ws_need = lib.hs_workspace_bytes(64)
     # nseg out of range, threshold outside (0, 1), missing workspace
-    assert step(p, N.u64p(b), N.u64p(e), 0, p, 4, 0.45, 1, 0, p, p, p, p, p, ws_need, None) == N.HS_ERR_INVALID_ARG
-    assert step(p, N.u64p(b), N.u64p(e), 65, p, 4, 0.45, 1, 0, p, p, p, p, p, ws_need, None) == N.HS_ERR_INVALID_ARG
-    assert step(p, N.u64p(b), N.u64p(e), 1, p, 4, 1.0, 1, 0, p, p, p, p, p, ws_need, None) == N.HS_ERR_INVALID_ARG
-    assert step(p, N.u64p(b), N.u64p(e), 1, p, 4, 0.45, 0, 0, p, p, p, p, p, ws_need, None) == N.HS_ERR_INVALID_ARG
-    assert step(p, N.u64p(b), N.u64p(e), 1, p, 4, 0.45, 1, 0, p, p, p, p, None, 0, None) == N.HS_ERR_WORKSPACE
+    assert step(p, N.u64p(b), N.u64p(e), 0, p, 4, 0.45, 1, 0, p, p, p, p, None, p, ws_need, None) == N.HS_ERR_INVALID_ARG
+    assert step(p, N.u64p(b), N.u64p(e), 65, p, 4, 0.45, 1, 0, p, p, p, p, None, p, ws_need, None) == N.HS_ERR_INVALID_ARG
+    assert step(p, N.u64p(b), N.u64p(e), 1, p, 4, 1.0, 1, 0, p, p, p, p, None, p, ws_need, None) == N.HS_ERR_INVALID_ARG
+    assert step(p, N.u64p(b), N.u64p(e), 1, p, 4, 0.45, 0, 0, p, p, p, p, None, p, ws_need, None) == N.HS_ERR_INVALID_ARG
+    assert step(p, N.u64p(b), N.u64p(e), 1, p, 4, 0.45, 1, 0, p, p, p, p, None, None, 0, None) == N.HS_ERR_WORKSPACE
     e6 = np.full(1, 6, np.uint64)
-    assert step(p, N.u64p(b), N.u64p(e6), 1, p, 4, 0.45, 1, 0, p, p, p, p, p, ws_need, None) == N.HS_ERR_ALIGNMENT
+    assert step(p, N.u64p(b), N.u64p(e6), 1, p, 4, 0.45, 1, 0, p, p, p, p, None, p, ws_need, None) == N.HS_ERR_ALIGNMENT
+    q = ctypes.c_void_p(264)  # 8-aligned: the fold's 16-B moves need 16
+    assert step(p, N.u64p(b), N.u64p(e), 1, p, 4, 0.45, 1, 0, q, p, p, p, None, p, ws_need, None) == N.HS_ERR_ALIGNMENT
+    assert step(p, N.u64p(b), N.u64p(e), 1, q, 4, 0.45, 1, 0, p, p, p, p, None, p, ws_need, None) == N.HS_ERR_ALIGNMENT
 
 
 def test_streaming_loop_sass_is_clean():
