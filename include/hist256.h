@@ -51,6 +51,10 @@ extern "C" {
 /* ---- kernel kinds (kernels.py:42-52 KernelKind) ------------------------- */
 #define HS_KIND_NAIVE 0      /* NVHist analogue, kernels.py:336-346 */
 #define HS_KIND_ADAPTIVE 1   /* AHist analogue,  kernels.py:349-384 */
+/* OR-ed into kind with HS_KIND_ADAPTIVE: the caller knows the pattern's prior is not
+ * dominated by one value (max-bin share below ~0.999), so the register path for the hot
+ * bin would not pay and the plain lane core runs. Counts are identical either way. */
+#define HS_KIND_FLAG_SPREAD 0x100
 
 /* ---- device strategies behind a kind --------------------- */
 #define HS_IMPL_AUTO 0       /* library picks by kind and size                     */
@@ -85,7 +89,8 @@ size_t hs_workspace_bytes(int nseg);
  * Replaces batch_histograms (stream.py:260-316), which drives _naive_worker
  * (kernels.py:97-130) / _adaptive_worker (kernels.py:133-168) per slice and
  * merges group partials (core.py:152-156). One launch for the whole batch.
- *   kind     HS_KIND_NAIVE or HS_KIND_ADAPTIVE (ADAPTIVE requires the pattern)
+ *   kind     HS_KIND_NAIVE or HS_KIND_ADAPTIVE (ADAPTIVE requires the pattern),
+ *            optionally | HS_KIND_FLAG_SPREAD
  *   impl     HS_IMPL_* (HS_IMPL_AUTO for production)
  *   h_offset/h_count: the CPU binning pattern (pattern.py:94-133), may be NULL
  *            for NAIVE; validated before launch (kernels.py:363).

@@ -35,6 +35,7 @@ HS_ERR_CUDA_BASE = -1000
 
 HS_KIND_NAIVE = 0
 HS_KIND_ADAPTIVE = 1
+HS_KIND_FLAG_SPREAD = 0x100
 
 HS_IMPL_AUTO = 0
 HS_IMPL_LANE = 1

@@ -1120,6 +1120,8 @@ int hs_histogram_batched(const uint8_t* d_data, const uint64_t* h_begin, const u
                          void* stream) {
   (void)d_ws; (void)ws_bytes;
   if (nseg < 0 || (nseg > 0 && (!h_begin || !h_end || !d_out))) return HS_ERR_INVALID_ARG;
+  const bool spread = (kind & HS_KIND_FLAG_SPREAD) != 0;
+  kind &= ~HS_KIND_FLAG_SPREAD;
   if (kind != HS_KIND_NAIVE && kind != HS_KIND_ADAPTIVE) return HS_ERR_INVALID_ARG;
   if (impl < HS_IMPL_AUTO || impl > HS_IMPL_SUBBIN) return HS_ERR_INVALID_ARG;
   PatternParams pp;
@@ -1129,6 +1131,7 @@ int hs_histogram_batched(const uint8_t* d_data, const uint64_t* h_begin, const u
   if (have_pattern) {
     int rc = make_pattern(h_offset, h_count, total_slots, cap, pp);
     if (rc != HS_OK) return rc;
+    if (spread) pp.hot_unique = 0;  // caller's hint: no dominant value in the prior
   }
   uint64_t total = 0;
   for (int s = 0; s < nseg; ++s) {

@@ -226,6 +226,13 @@ def _pattern_args(pattern):
     return N.i64p(off), N.i64p(cnt), int(pattern.total_slots), int(pattern.cap), (off, cnt)
 
 
+# ADAPTIVE takes the register path for the hot bin only when the prior's max-bin share
+# reaches this. The path skips a warp's atomics only when all 32 lanes hold an all-hot
+# 16-byte vector, P = share^512 (0.60 at 0.999); below that the per-vector test and the
+# 768-thread CTAs cost 3-4% (profiles/paper_tables_b200.md Fig. 5: no gain even at 0.99)
+SPREAD_BELOW = 0.999
+
+
 def launch(staged: StagedBatch, kind: int, pattern=None, stream=None, impl: int = N.HS_IMPL_AUTO, out=None,
            staging: Staging | None = None):
     """hs_histogram_batched on ``stream`` (waits for the staging copies first): one
@@ -241,6 +248,9 @@ def launch(staged: StagedBatch, kind: int, pattern=None, stream=None, impl: int 
         with t.cuda.stream(stream):
             out = t.empty((max(nseg, 1), BINS), dtype=t.int64, device=t.cuda.current_device())
     off_p, cnt_p, S, cap, keep = _pattern_args(pattern)
+    dom = getattr(pattern, "dominance", None)
+    if kind == N.HS_KIND_ADAPTIVE and dom is not None and dom < SPREAD_BELOW:
+        kind |= N.HS_KIND_FLAG_SPREAD
     begin = np.ascontiguousarray(staged.begin, dtype=np.uint64)
     end = np.ascontiguousarray(staged.end, dtype=np.uint64)
     status = N.lib().hs_histogram_batched(
