@@ -315,3 +315,34 @@ def test_ticketed_output_matches_atomic_output(cuda, oracle):
                 assert np.array_equal(out.cpu().numpy().view(np.uint64), want), (trial, kind, use_ws)
     # every launch leaves the workspace (tickets and accumulator rows) zero again
     assert int(ws.sum().item()) == 0
+
+
+@pytest.mark.parametrize("p", [0.5, 0.99, 0.9995])
+def test_register_path_on_partially_hot_data(cuda, oracle, p):
+    """The ADAPTIVE register path (hot bin counted per all-hot 16-byte vector) forced on
+    mixtures where only some vectors are all hot, at sizes with head/tail words and a
+    remainder; and the API's choice (spread hint below dominance 0.999) on the same
+    data. Both exact."""
+    torch = cuda
+    n = (1 << 22) + 4 * 37
+    host = oracle.generate("mixture", n, 11, value=200, degeneracy=p)
+    want = oracle.histogram(host)
+    buf = torch.from_numpy(host.copy()).cuda()
+    pat = deg_pattern(200)  # unique widest run at 200: hot_unique, dominance 1.0
+    L = N.lib()
+    for off in (0, 4, 12):
+        seg = buf[off:n - 8]
+        exp = oracle.histogram(host[off:n - 8])
+        b0 = np.zeros(1, np.uint64)
+        b1 = np.full(1, seg.numel(), np.uint64)
+        out = torch.empty((1, 256), dtype=torch.int64, device="cuda")
+        ws = D.default_staging().workspace()
+        for kind in (N.HS_KIND_ADAPTIVE, N.HS_KIND_ADAPTIVE | N.HS_KIND_FLAG_SPREAD):
+            N.check(L.hs_histogram_batched(seg.data_ptr(), N.u64p(b0), N.u64p(b1), 1, kind, N.HS_IMPL_LANE,
+                                           N.i64p(pat.offset), N.i64p(pat.count), 960, 8, out.data_ptr(),
+                                           ws.data_ptr(), ws.numel(), torch.cuda.current_stream().cuda_stream), "h")
+            assert out.cpu().numpy().view(np.uint64)[0].tolist() == exp.tolist(), (p, off, kind)
+    prior = hs.compute_binning_pattern(hs.Histogram256(want))
+    assert (prior.dominance >= D.SPREAD_BELOW) == (p >= 0.999)
+    got = hs.adaptive_histogram(hs.DeviceChunk(buf), prior, hs.WorkerGroupConfig())
+    assert got.counts.tolist() == want.tolist()

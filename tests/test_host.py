@@ -248,3 +248,16 @@ def test_report_csv_format():
     assert lines[0].endswith(",degeneracy,divergence")
     assert lines[1] == "0,1.000,2.000,3.000,4.000,5.000,naive,0.500000,0.250000"
     assert lines[2] == "summary,15.000,15.000,100.00,,,,,"
+
+
+def test_pattern_dominance_hint():
+    """compute_binning_pattern records the prior's max-bin share (an extension used to
+    choose the ADAPTIVE register path); it does not take part in equality."""
+    c = np.zeros(256, np.uint64)
+    c[7], c[9] = 3, 1
+    p = hs.compute_binning_pattern(hs.Histogram256(c))
+    assert p.dominance == 0.75
+    assert hs.compute_binning_pattern(hs.Histogram256(np.zeros(256, np.uint64))).dominance == 0.0
+    assert hs.uniform_pattern(960).dominance is None
+    q = hs.BinningPattern(p.offset, p.count, p.total_slots, p.cap)
+    assert q == p and q.dominance is None
