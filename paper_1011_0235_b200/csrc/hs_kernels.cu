@@ -41,6 +41,10 @@ struct SegParams {
   uint64_t vstart[kMaxSeg + 1];  // virtual (concatenated) start of segment s
   int nseg;
   int out_base;                  // index of segment 0 of this launch in d_out
+  // balanced split of the concatenated words over the grid, precomputed on the host
+  // (no 64-bit division on the device): CTA b owns q words, plus one if b < r
+  uint64_t q, r;
+  uint32_t ctas_after_first[kMaxSeg];  // (last CTA - first CTA) touching segment s
 };
 
 struct PatternParams {
@@ -126,13 +130,19 @@ __device__ __forceinline__ void block_range(uint64_t total, uint64_t& vb, uint64
   ve = vb + 4 * (q + (b < r ? 1 : 0));
 }
 
+// The same split with the host's q, r (SegParams launches)
+__device__ __forceinline__ void block_range(const SegParams& sp, uint64_t& vb, uint64_t& ve) {
+  const uint64_t b = blockIdx.x;
+  vb = 4 * (sp.q * b + min(b, sp.r));
+  ve = vb + 4 * (sp.q + (b < sp.r ? 1 : 0));
+}
+
 // Walks the pieces (segment index, device byte range) of the block's range and calls
 // body(seg, p0, p1) for each non-empty piece; body must end with a block-wide flush.
 template <uint64_t kCap, class Body>
 __device__ __forceinline__ void for_each_piece(const SegParams& sp, Body&& body) {
-  const uint64_t total = sp.vstart[sp.nseg];
   uint64_t vb, ve;
-  block_range(total, vb, ve);
+  block_range(sp, vb, ve);
   if (vb >= ve) return;
   int s = 0;
   while (s < sp.nseg && sp.vstart[s + 1] <= vb) ++s;
@@ -245,12 +255,6 @@ struct Tickets {
   unsigned long long* acc;       // [kMaxSeg][256], zero on entry and on exit
 };
 
-// CTA index owning word w of the balanced split (inverse of block_range)
-__device__ __forceinline__ uint32_t cta_of_word(uint64_t w, uint64_t tw, uint32_t g) {
-  const uint64_t q = tw / g, r = tw % g;
-  if (w < r * (q + 1)) return uint32_t(w / (q + 1));
-  return uint32_t(r + (w - r * (q + 1)) / q);
-}
 
 // Adds the CTA's counters into dst[256] (the output row, or the segment's accumulator
 // row of a ticketed launch) and re-zeroes them: 4 threads per bin, each summing 8 of
@@ -258,7 +262,7 @@ __device__ __forceinline__ uint32_t cta_of_word(uint64_t w, uint64_t tw, uint32_
 // a mid-range flush must not wait for its REDs to reach L2 (that round trip under a
 // saturated memory system was ~6 us per CTA; tools/ab_seg.py), so the fence and the
 // tickets are taken once per CTA at the end (lane_tickets).
-__device__ __forceinline__ void lane_flush(uint32_t sbase, unsigned long long* __restrict__ dst) {
+__device__ __forceinline__ void lane_flush(uint32_t sbase, unsigned long long* __restrict__ dst, bool rezero) {
   compiler_fence();
   __syncthreads();
   pdl_wait();  // the previous launch on this stream may still own the workspace / outputs
@@ -269,7 +273,7 @@ __device__ __forceinline__ void lane_flush(uint32_t sbase, unsigned long long* _
     for (int i = 0; i < 8; ++i) {
       const uint32_t a = sbase + b * 128 + (((sub * 8 + i + b) & 31) << 2);
       v += sh_ld(a);
-      sh_st(a, 0);
+      if (rezero) sh_st(a, 0);  // not after the CTA's last piece
     }
     unsigned long long tot = v;
     tot += __shfl_xor_sync(0xffffffffu, tot, 1);
@@ -290,13 +294,10 @@ __device__ __forceinline__ void lane_tickets(const Tickets& tk, const SegParams&
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
-    const uint64_t tw = sp.vstart[sp.nseg] >> 2;
     unsigned long long m = 0;
     for (int s = s_first; s <= s_last; ++s) {
       if (sp.vstart[s + 1] == sp.vstart[s]) continue;  // empty: no CTA owns it
-      const uint32_t c0 = cta_of_word(sp.vstart[s] >> 2, tw, gridDim.x);
-      const uint32_t c1 = cta_of_word((sp.vstart[s + 1] >> 2) - 1, tw, gridDim.x);
-      if (atomicAdd(tk.ticket + s, 1u) == c1 - c0) m |= 1ull << s;
+      if (atomicAdd(tk.ticket + s, 1u) == sp.ctas_after_first[s]) m |= 1ull << s;
     }
     lastmask = m;
   }
@@ -451,7 +452,7 @@ __global__ void __launch_bounds__(TH, kLaneMinBlocks)
     lane_piece<U, HOT, TH>(data, pc_p0[i], pc_p1[i], tb, hot4);
     HS_STAMP(2 + 2 * i);
     const int s = pc_seg[i];
-    lane_flush(sbase, ticketed ? tk.acc + size_t(s) * 256 : out + size_t(sp.out_base + s) * 256);
+    lane_flush(sbase, ticketed ? tk.acc + size_t(s) * 256 : out + size_t(sp.out_base + s) * 256, i + 1 < pc_n);
     HS_STAMP(3 + 2 * i);
   }
   if (ticketed && pc_n > 0) lane_tickets(tk, sp, pc_seg[0], pc_seg[pc_n - 1], out);
@@ -999,6 +1000,25 @@ int set_smem(K kernel, size_t bytes) {
   return fold(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
 }
 
+// CTA index owning word w of the balanced split of tw words over g CTAs
+uint32_t cta_of_word(uint64_t w, uint64_t tw, uint64_t g) {
+  const uint64_t q = tw / g, r = tw % g;
+  if (w < r * (q + 1)) return uint32_t(w / (q + 1));
+  return uint32_t(r + (w - r * (q + 1)) / q);
+}
+
+// fills the grid split of sp (q, r and the per-segment CTA spans the tickets count)
+void split_grid(SegParams& sp, int grid) {
+  const uint64_t tw = sp.vstart[sp.nseg] >> 2, g = uint64_t(grid);
+  sp.q = tw / g;
+  sp.r = tw % g;
+  for (int s = 0; s < sp.nseg; ++s) {
+    sp.ctas_after_first[s] = 0;
+    if (sp.vstart[s + 1] > sp.vstart[s])
+      sp.ctas_after_first[s] = cta_of_word((sp.vstart[s + 1] >> 2) - 1, tw, g) - cta_of_word(sp.vstart[s] >> 2, tw, g);
+  }
+}
+
 // one launch over <= kMaxSeg segments
 int launch_batch(const uint8_t* d_data, const uint64_t* h_begin, const uint64_t* h_end, int s0, int ns,
                  int kind, int impl, const PatternParams* pp, unsigned long long* d_out, cudaStream_t st,
@@ -1022,12 +1042,12 @@ int launch_batch(const uint8_t* d_data, const uint64_t* h_begin, const uint64_t*
     // one while the next histogram streams, instead of delaying one of its CTAs)
     const int grid = int(std::max<uint64_t>(
         1, std::min<uint64_t>(want, uint64_t(di.sms) * kLaneMinBlocks - uint64_t(reserve_slots))));
+    split_grid(sp, grid);
     const int hb = pp ? pp->hot_bin : 0;
     // ADAPTIVE runs the register path for the pattern's hot bin only when the pattern
-    // marks a dominant value (unique widest sub-bin run): its per-vector test costs ~2%
-    // on spread data and gains on degenerate data. The HOT form uses 768-thread CTAs
-    // (40 registers): at 1024 threads its loop spills under the 32-register budget.
-    // The device stream engine always runs the HOT form (its kind is decided on the GPU).
+    // marks a dominant value (unique widest sub-bin run, and no HS_KIND_FLAG_SPREAD
+    // from the caller). The HOT form uses 768-thread CTAs (40 registers): at 1024
+    // threads its loop spills under the 32-register budget.
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.stream = st;
@@ -1049,6 +1069,7 @@ int launch_batch(const uint8_t* d_data, const uint64_t* h_begin, const uint64_t*
   } else if (impl == HS_IMPL_WARP) {
     const uint64_t want = (v + (32ull << 10) - 1) / (32ull << 10);
     const int grid = int(std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(di.sms) * 8)));
+    split_grid(sp, grid);
     k_warp<4, 0><<<grid, kWarpThreads, 0, st>>>(d_data, sp, d_out);
   } else if (impl == HS_IMPL_SUBBIN) {
     if (!pp) return HS_ERR_INVALID_ARG;
@@ -1059,6 +1080,7 @@ int launch_batch(const uint8_t* d_data, const uint64_t* h_begin, const uint64_t*
     const uint64_t want = (v + (64ull << 10) - 1) / (64ull << 10);
     const int per_sm = std::max(1, int(di.smem_optin / (smem + 1024)));
     const int grid = int(std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(di.sms) * per_sm)));
+    split_grid(sp, grid);
     k_subbin<4, 0><<<grid, kSubThreads, smem, st>>>(d_data, sp, *pp, d_out);
   } else {
     return HS_ERR_INVALID_ARG;
