@@ -455,7 +455,12 @@ def main(argv=None):
         cpu = cpu_baseline(streams, args.cpu_seconds)
 
     extra = {}
+    if not args.no_extras:
+        c5 = c5_sharded(hs, N, torch, L, dev, rank, world)
+        del streams[:]  # free the step inputs before the larger extras
+        torch.cuda.empty_cache()
     if rank == 0 and not args.no_extras:
+        extra["c5_64gib_sharded"] = c5
         extra["c1_image_1024x1024"] = c1_image(hs, N, torch, L, dev)
         extra["c3_switch_stream"] = c3_switch(hs, torch, dev)
 
@@ -559,6 +564,56 @@ def c1_image(hs, N, torch, L, dev):
             "batched_64_images_us_per_image": round(batch_us / 64, 3),
             "batched_64_images_gbs": round(64 * n / (batch_us * 1e3), 1),
             "graph_single_image_us": round(graph_us, 3), "cpu_reference_port_us": round(cpu_us, 1)}
+
+
+C5_BYTES = 64 << 30  # BASELINE configs[4]: 64 GiB device-resident, sharded over the GPUs
+
+
+def c5_sharded(hs, N, torch, L, dev, rank, world):
+    """BASELINE configs[4]: a 64 GiB uniform stream sharded by contiguous byte range
+    (the group_ranges rule) across the ranks, generated in place on each GPU; each rank
+    counts its 64/N GiB in one launch (64 segments) and one NCCL all_reduce joins the
+    counts. Strong scaling: GB/s = 64 GiB / max-over-ranks device time (median of 3)."""
+    from paper_1011_0235_b200.distributed import shard_range
+
+    lo, hi = shard_range(C5_BYTES, rank, world)  # bytes
+    n = hi - lo
+    buf = torch.empty(n, dtype=torch.uint8, device=dev)
+    hs.generate_device(hs.SourceSpec("uniform", C5_BYTES, BASE_SEED ^ 0xC5), buf, first_pixel=lo)
+    nseg = 64
+    edges = np.linspace(0, n // 4, nseg + 1).astype(np.uint64) * np.uint64(4)
+    begin, end = edges[:-1].copy(), edges[1:].copy()
+    out = torch.empty((nseg, 256), dtype=torch.int64, device=dev)
+    ws = torch.zeros(int(L.hs_workspace_bytes(nseg)), dtype=torch.uint8, device=dev)
+    total = torch.empty(256, dtype=torch.int64, device=dev)
+    st = torch.cuda.current_stream()
+
+    def once():
+        N.check(L.hs_histogram_batched(buf.data_ptr(), N.u64p(begin), N.u64p(end), nseg, N.HS_KIND_NAIVE,
+                                       N.HS_IMPL_AUTO, None, None, 0, 0, out.data_ptr(), ws.data_ptr(), ws.numel(),
+                                       st.cuda_stream), "c5")
+        torch.sum(out, dim=0, out=total)
+        if _dist_on():
+            torch.distributed.all_reduce(total)
+
+    once()
+    times = []
+    for _ in range(3):
+        torch.cuda.synchronize()
+        barrier(world)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        once()
+        b.record()
+        b.synchronize()
+        times.append(max_over_ranks(a.elapsed_time(b), world))
+    ms = float(np.median(times))
+    assert int(total.sum().item()) == C5_BYTES, "c5 total"
+    del buf
+    torch.cuda.empty_cache()
+    return {"bytes": C5_BYTES, "per_gpu_bytes": n, "n_gpus": world, "ms": round(ms, 3),
+            "gbs": round(C5_BYTES / (ms / 1e3) / 1e9, 1), "data": "uniform, generated in place per shard",
+            "collective": "nccl all_reduce of 256 counts" if _dist_on() else "none (single process)"}
 
 
 def c3_switch(hs, torch, dev):

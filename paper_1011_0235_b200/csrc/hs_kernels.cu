@@ -41,6 +41,10 @@ struct SegParams {
   uint64_t vstart[kMaxSeg + 1];  // virtual (concatenated) start of segment s
   int nseg;
   int out_base;                  // index of segment 0 of this launch in d_out
+  int acc_base;                  // its workspace accumulator row / ticket index
+  // segments that continue in the next launch of the same call (bit s): their CTAs
+  // only RED into the accumulator row; the launch holding a segment's end finalizes it
+  unsigned long long open_mask;
   // balanced split of the concatenated words over the grid, precomputed on the host
   // (no 64-bit division on the device): CTA b owns q words, plus one if b < r
   uint64_t q, r;
@@ -297,7 +301,8 @@ __device__ __forceinline__ void lane_tickets(const Tickets& tk, const SegParams&
     unsigned long long m = 0;
     for (int s = s_first; s <= s_last; ++s) {
       if (sp.vstart[s + 1] == sp.vstart[s]) continue;  // empty: no CTA owns it
-      if (atomicAdd(tk.ticket + s, 1u) == sp.ctas_after_first[s]) m |= 1ull << s;
+      if ((sp.open_mask >> s) & 1) continue;            // finalized by a later launch
+      if (atomicAdd(tk.ticket + sp.acc_base + s, 1u) == sp.ctas_after_first[s]) m |= 1ull << s;
     }
     lastmask = m;
   }
@@ -309,8 +314,8 @@ __device__ __forceinline__ void lane_tickets(const Tickets& tk, const SegParams&
       const int s = __ffsll(m) - 1;
       m &= m - 1;
       for (uint32_t b = threadIdx.x; b < 256; b += blockDim.x)
-        out[size_t(sp.out_base + s) * 256 + b] = atomicExch(tk.acc + size_t(s) * 256 + b, 0ull);
-      if (threadIdx.x == 0) tk.ticket[s] = 0;
+        out[size_t(sp.out_base + s) * 256 + b] = atomicExch(tk.acc + size_t(sp.acc_base + s) * 256 + b, 0ull);
+      if (threadIdx.x == 0) tk.ticket[sp.acc_base + s] = 0;
     }
   }
 }
@@ -452,7 +457,8 @@ __global__ void __launch_bounds__(TH, kLaneMinBlocks)
     lane_piece<U, HOT, TH>(data, pc_p0[i], pc_p1[i], tb, hot4);
     HS_STAMP(2 + 2 * i);
     const int s = pc_seg[i];
-    lane_flush(sbase, ticketed ? tk.acc + size_t(s) * 256 : out + size_t(sp.out_base + s) * 256, i + 1 < pc_n);
+    lane_flush(sbase, ticketed ? tk.acc + size_t(sp.acc_base + s) * 256 : out + size_t(sp.out_base + s) * 256,
+               i + 1 < pc_n);
     HS_STAMP(3 + 2 * i);
   }
   if (ticketed && pc_n > 0) lane_tickets(tk, sp, pc_seg[0], pc_seg[pc_n - 1], out);
@@ -1019,20 +1025,11 @@ void split_grid(SegParams& sp, int grid) {
   }
 }
 
-// one launch over <= kMaxSeg segments
-int launch_batch(const uint8_t* d_data, const uint64_t* h_begin, const uint64_t* h_end, int s0, int ns,
-                 int kind, int impl, const PatternParams* pp, unsigned long long* d_out, cudaStream_t st,
-                 const DevInfo& di, const Tickets& tk, int reserve_slots = 0) {
-  SegParams sp;
-  sp.nseg = ns;
-  sp.out_base = s0;
-  uint64_t v = 0;
-  for (int i = 0; i < ns; ++i) {
-    sp.begin[i] = h_begin[s0 + i];
-    sp.vstart[i] = v;
-    v += h_end[s0 + i] - h_begin[s0 + i];
-  }
-  sp.vstart[ns] = v;
+// one launch over the <= kMaxSeg (pieces of) segments prepared in sp
+int launch_batch(const uint8_t* d_data, SegParams& sp, int kind, int impl, const PatternParams* pp,
+                 unsigned long long* d_out, cudaStream_t st, const DevInfo& di, const Tickets& tk,
+                 int reserve_slots = 0) {
+  const uint64_t v = sp.vstart[sp.nseg];
   if (v == 0) return HS_OK;
   cudaError_t e = cudaSuccess;
   if (impl == HS_IMPL_LANE) {
@@ -1088,6 +1085,53 @@ int launch_batch(const uint8_t* d_data, const uint64_t* h_begin, const uint64_t*
   e = cudaGetLastError();
   return fold(e);
 }
+
+// Segments [s0, s0 + ns) as launches of at most kLaunchBytes each. A single launch over
+// many GiB lets the two CTAs of an SM drift apart (the exits of a 16 GiB launch spread
+// from 57% to 100% of its time; tools/trace_lane.py), and the SM idles once its faster
+// CTA is done. Consecutive <= 1 GiB launches with programmatic dependent launch refill
+// those slots with the next launch's CTAs (tools/ablib/footprint.py: 64 x 1 GiB launches
+// 6.53 TB/s, 1 x 64 GiB 5.50 TB/s). A segment cut by a launch boundary accumulates in
+// its workspace row (or, without a workspace, in d_out after the memset) and is
+// finalized by the launch that holds its end.
+constexpr uint64_t kLaunchBytes = 1ull << 30;  // a word multiple, so every cut is word aligned
+
+int launch_segments(const uint8_t* d_data, const uint64_t* h_begin, const uint64_t* h_end, int s0, int ns,
+                    int kind, int impl, const PatternParams* pp, unsigned long long* d_out, cudaStream_t st,
+                    const DevInfo& di, const Tickets& tk, int reserve_slots = 0) {
+  uint64_t vs[kMaxSeg + 1];
+  vs[0] = 0;
+  for (int i = 0; i < ns; ++i) vs[i + 1] = vs[i] + (h_end[s0 + i] - h_begin[s0 + i]);
+  const uint64_t total = vs[ns];
+  if (total == 0) return HS_OK;
+  for (uint64_t v0 = 0; v0 < total; v0 += kLaunchBytes) {
+    const uint64_t v1 = std::min(total, v0 + kLaunchBytes);
+    const bool last = v1 == total;
+    SegParams sp;
+    sp.nseg = 0;
+    sp.open_mask = 0;
+    sp.acc_base = -1;
+    for (int i = 0; i < ns; ++i) {
+      // a non-empty segment joins every launch it intersects; an empty one the launch
+      // holding its position (the last launch for positions at the very end)
+      const bool empty = vs[i + 1] == vs[i];
+      const bool in = empty ? (vs[i] >= v0 && (vs[i] < v1 || last)) : (vs[i] < v1 && vs[i + 1] > v0);
+      if (!in) continue;
+      if (sp.acc_base < 0) sp.acc_base = i;  // members are consecutive indices
+      const uint64_t a = std::max(vs[i], v0), b = std::min(vs[i + 1], v1);
+      const int k = sp.nseg++;
+      sp.begin[k] = h_begin[s0 + i] + (empty ? 0 : a - vs[i]);
+      sp.vstart[k] = (empty ? std::min(vs[i], v1) : a) - v0;
+      sp.vstart[k + 1] = (empty ? std::min(vs[i], v1) : b) - v0;
+      if (vs[i + 1] > v1) sp.open_mask |= 1ull << k;
+    }
+    sp.out_base = s0 + sp.acc_base;
+    int rc = launch_batch(d_data, sp, kind, impl, pp, d_out, st, di, tk, reserve_slots);
+    if (rc != HS_OK) return rc;
+  }
+  return HS_OK;
+}
+
 
 }  // namespace
 
@@ -1187,8 +1231,8 @@ int hs_histogram_batched(const uint8_t* d_data, const uint64_t* h_begin, const u
       if (e != cudaSuccess) return fold(e);
       continue;
     }
-    rc = launch_batch(d_data, h_begin, h_end, s0, ns, kind, impl, have_pattern ? &pp : nullptr,
-                      reinterpret_cast<unsigned long long*>(d_out), st, di, tk);
+    rc = launch_segments(d_data, h_begin, h_end, s0, ns, kind, impl, have_pattern ? &pp : nullptr,
+                         reinterpret_cast<unsigned long long*>(d_out), st, di, tk);
     if (rc != HS_OK) return rc;
   }
   return HS_OK;
@@ -1317,8 +1361,8 @@ int hs_stream_step(const uint8_t* d_data, const uint64_t* h_begin, const uint64_
     // The histogram does not wait for the previous fold's decision: both kinds count
     // exactly the same, so the lane kernel runs for either and streams while the fold
     // (one CTA) finishes on the side; the decided kind is what the log records.
-    rc = launch_batch(d_data, h_begin, h_end, 0, nseg, HS_KIND_NAIVE, HS_IMPL_LANE, nullptr,
-                      reinterpret_cast<unsigned long long*>(d_out), st, di, tk, /*reserve_slots=*/1);
+    rc = launch_segments(d_data, h_begin, h_end, 0, nseg, HS_KIND_NAIVE, HS_IMPL_LANE, nullptr,
+                         reinterpret_cast<unsigned long long*>(d_out), st, di, tk, /*reserve_slots=*/1);
     if (rc != HS_OK) return rc;
   }
   // pattern and kernel refresh for iteration+1 when (iteration+1) % every == 0 (stream.py:407-414)

@@ -91,3 +91,31 @@ def test_bench_configuration_per_chunk(cuda, oracle):
     got = hs.batch_histograms(chunks, hs.KernelKind.ADAPTIVE, pat, hs.WorkerGroupConfig())
     assert np.array_equal(np.stack([g.counts for g in got]), want)
     del buf
+
+
+def test_large_launch_across_segments(cuda, oracle):
+    """A 3 GiB call is cut into <= 1 GiB launches; segments of irregular sizes -- tiny,
+    empty, and larger than a launch -- cross launch boundaries and accumulate across
+    them. Every segment's counts equal the host's, ticketed and memset+RED alike."""
+    torch = cuda
+    n = 3 * GiB + 64
+    buf = torch.empty(n, dtype=torch.uint8, device="cuda")
+    hs.generate_device(hs.SourceSpec("normal", n, 21, mean=128.0, sigma=40.0), buf)
+    host = buf.cpu().numpy()
+    cuts = [0, 700 << 20, (700 << 20) + 12, (700 << 20) + 12, (2300 << 20) + 4, n - 8, n]
+    begin = np.array(cuts[:-1], np.uint64)
+    end = np.array(cuts[1:], np.uint64)
+    want = [oracle.histogram(host[a:b]) for a, b in zip(cuts[:-1], cuts[1:])]
+    L = N.lib()
+    out = torch.empty((len(want), 256), dtype=torch.int64, device="cuda")
+    ws = D.default_staging().workspace()
+    for use_ws in (True, False):
+        out.fill_(-1)
+        N.check(L.hs_histogram_batched(buf.data_ptr(), N.u64p(begin), N.u64p(end), len(want), N.HS_KIND_NAIVE,
+                                       N.HS_IMPL_LANE, None, None, 0, 0, out.data_ptr(),
+                                       ws.data_ptr() if use_ws else None, ws.numel() if use_ws else 0,
+                                       torch.cuda.current_stream().cuda_stream), "rounds")
+        got = out.cpu().numpy().view(np.uint64)
+        for s, w in enumerate(want):
+            assert got[s].tolist() == w.tolist(), (use_ws, s)
+    assert not ws.any().item()  # tickets and accumulator rows are zero again

@@ -17,9 +17,10 @@ from paper_1011_0235_b200 import _native as N  # noqa: E402
 L = N.lib()
 raw = ctypes.CDLL(os.environ["HS_LIBHIST256"])
 nseg = int(sys.argv[1]) if len(sys.argv) > 1 else 64
-n = 1 << 30
+n = (int(sys.argv[2]) if len(sys.argv) > 2 else 1024) << 20
 st = torch.cuda.current_stream()
 buf = torch.empty(n, dtype=torch.uint8, device="cuda")
+reps = int(sys.argv[3]) if len(sys.argv) > 3 else 10
 hs.generate_device(hs.SourceSpec("normal", n, 5, mean=128.0, sigma=32.0), buf)
 ws = torch.zeros(int(L.hs_workspace_bytes(64)), dtype=torch.uint8, device="cuda")
 out = torch.empty((64, 256), dtype=torch.int64, device="cuda")
@@ -37,7 +38,7 @@ for _ in range(3):
 torch.cuda.synchronize()
 raw.hs_trace_clear()
 torch.cuda._sleep(20_000_000)
-for _ in range(10):
+for _ in range(reps):
     call()
 torch.cuda.synchronize()
 t = np.zeros((1024, 16), np.uint64)
@@ -62,3 +63,13 @@ for i in range(3):
 last = np.array([max(rel[c, 3 + 2 * i] for i in range(7) if t[c, 3 + 2 * i] > 0) for c in range(g)])
 print(f"  tickets    mean {np.mean(rel[:, 15] - last):.2f} us")
 print(f"  CTA exit   min {rel[:, 15].min():.1f} max {rel[:, 15].max():.1f} us")
+loop0 = rel[:, 2] - rel[:, 1]
+print(f"  loop (thread 0) per CTA: min {loop0.min():.2f} median {np.median(loop0):.2f} max {loop0.max():.2f} us")
+print(f"  start->loop begin (zero + piece list): median {np.median(rel[:, 1] - rel[:, 0]):.2f} us")
+print(f"  last piece end -> exit (flush + tickets): median {np.median(rel[:, 15] - rel[:, 2]):.2f} "
+      f"max {np.max(rel[:, 15] - rel[:, 2]):.2f} us")
+ex = rel[:, 15]
+print(f"  CTA exit spread: p10 {np.percentile(ex, 10):.1f} p50 {np.percentile(ex, 50):.1f} p90 {np.percentile(ex, 90):.1f} max {ex.max():.1f} us")
+sm = np.array([0] * g)
+hist = np.histogram(rel[:, 0], bins=8)
+print("  CTA start histogram (us edges, counts):", [round(e, 1) for e in hist[1]], hist[0].tolist())
