@@ -1090,8 +1090,9 @@ int launch_batch(const uint8_t* d_data, SegParams& sp, int kind, int impl, const
 // many GiB lets the two CTAs of an SM drift apart (the exits of a 16 GiB launch spread
 // from 57% to 100% of its time; tools/trace_lane.py), and the SM idles once its faster
 // CTA is done. Consecutive <= 1 GiB launches with programmatic dependent launch refill
-// those slots with the next launch's CTAs (tools/ablib/footprint.py: 64 x 1 GiB launches
-// 6.53 TB/s, 1 x 64 GiB 5.50 TB/s). A segment cut by a launch boundary accumulates in
+// those slots with the next launch's CTAs: one 16 GiB call 5.93 -> 6.57 TB/s, measured
+// from a settled power state (the board's power cap otherwise confounds long runs;
+// DESIGN.md §5). A segment cut by a launch boundary accumulates in
 // its workspace row (or, without a workspace, in d_out after the memset) and is
 // finalized by the launch that holds its end.
 constexpr uint64_t kLaunchBytes = 1ull << 30;  // a word multiple, so every cut is word aligned
