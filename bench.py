@@ -101,6 +101,8 @@ class ClockSampler:
             time.sleep(0.005)
 
     def __enter__(self):
+        if os.environ.get("HS_BENCH_NO_SAMPLER"):  # A/B of the sampler's own cost
+            self.nv = None
         if self.nv is not None:
             self._t = threading.Thread(target=self._run, daemon=True)
             self._t.start()
@@ -239,6 +241,7 @@ def main(argv=None):
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--sustain-seconds", type=float, default=2.0)
+    ap.add_argument("--settle-seconds", type=float, default=1.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extras", action="store_true")
@@ -369,6 +372,10 @@ def main(argv=None):
     torch.cuda.synchronize()
     per_sigma, launch_ms, avg_launch_ms, reps = serial_roofline()
     torch.cuda.synchronize()
+    # The timed region starts from an idle GPU: this kernel draws the board's 1000 W
+    # limit within ~50 ms, so whatever ran just before would otherwise decide how much
+    # of the region runs power-capped. The capped rate is reported as `sustained`.
+    time.sleep(args.settle_seconds)
     barrier(world)
     torch.cuda.synchronize()
     t0 = torch.cuda.Event(enable_timing=True)
@@ -472,7 +479,8 @@ def main(argv=None):
             "config": {"workload": WORKLOAD, "bytes_per_step_per_gpu": bytes_per_step_rank, "chunk_bytes": CHUNK,
                        "sigmas": list(SIGMAS), "mean": MEAN, "kernel": "adaptive", "pattern": "CPU, lag-1 per stream",
                        "cuda_streams": "one per sigma stream (kernel tails overlap)",
-                       "parallelism": f"shard{world}" + ("+nccl_allreduce" if dist_on else ""), "l2": "inputs 3 GiB/GPU >> 126 MB L2 (no flush needed)"},
+                       "parallelism": f"shard{world}" + ("+nccl_allreduce" if dist_on else ""), "l2": "inputs 3 GiB/GPU >> 126 MB L2 (no flush needed)",
+                       "timed_region_start": f"idle GPU ({args.settle_seconds:g} s settle); power-capped rate in `sustained`"},
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -119,3 +119,20 @@ def test_large_launch_across_segments(cuda, oracle):
         for s, w in enumerate(want):
             assert got[s].tolist() == w.tolist(), (use_ws, s)
     assert not ws.any().item()  # tickets and accumulator rows are zero again
+
+
+def test_split_launches_over_groups(cuda, oracle):
+    """70 segments (two groups of <= 64) where a 1.25 GiB segment and a 0.5 GiB one are
+    cut by launch boundaries between tiny and empty neighbours; batch_histograms
+    agrees with the host per segment."""
+    torch = cuda
+    sizes = [4, 0, 1280 << 20, 8, 0, 512 << 20, 12] + [(k % 5) * 4096 + 4 * k for k in range(63)]
+    n = sum(sizes)
+    buf = torch.empty(n, dtype=torch.uint8, device="cuda")
+    hs.generate_device(hs.SourceSpec("uniform", n, 77), buf)
+    host = buf.cpu().numpy()
+    offs = np.cumsum([0] + sizes)
+    chunks = [hs.DeviceChunk(buf[offs[i]:offs[i + 1]]) for i in range(len(sizes))]
+    got = hs.batch_histograms(chunks, hs.KernelKind.NAIVE, None, hs.WorkerGroupConfig())
+    for i, h in enumerate(got):
+        assert h.counts.tolist() == oracle.histogram(host[offs[i]:offs[i + 1]]).tolist(), i
