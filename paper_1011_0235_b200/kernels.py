@@ -121,7 +121,9 @@ def adaptive_histogram(chunk, pattern: BinningPattern, cfg: WorkerGroupConfig, *
     """AHist analogue (kernels.py:349-384).
 
     The pattern is validated before launch (kernels.py:363). The production launch
-    counts with the lane-private core and registers the pattern's hot bin; with
+    counts with the lane-banked core; when the pattern's prior was dominated by one
+    value (pattern.dominance >= device.SPREAD_BELOW, or for patterns of unknown origin a
+    unique widest sub-bin run) its hot bin is counted in registers. With
     ``return_slots`` or ``narrow_counters`` the reference's per-group slot arrays
     (group/lane mapping of kernels.py:105-108, :149-150) are produced on the device by
     hs_group_slots and reduced per bin as reduce_subbins does."""
