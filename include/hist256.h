@@ -108,6 +108,26 @@ int hs_histogram_batched(const uint8_t* d_data, const uint64_t* h_begin, const u
                          int64_t total_slots, int64_t cap,
                          uint64_t* d_out, void* d_ws, size_t ws_bytes, void* stream);
 
+/* hs_histogram_batched, then the D2H of d_out[nseg][256] into h_out and a wait for the
+ * stream: the synchronous API path for device-resident chunks in one call. Blocking. */
+int hs_histogram_sync(const uint8_t* d_data, const uint64_t* h_begin, const uint64_t* h_end, int nseg,
+                      int kind, int impl, const int64_t* h_offset, const int64_t* h_count,
+                      int64_t total_slots, int64_t cap, uint64_t* d_out, uint64_t* h_out,
+                      void* d_ws, size_t ws_bytes, void* stream);
+
+/* Synchronous convenience for host-resident chunks (the one-call naive_histogram /
+ * adaptive_histogram / batch_histograms path of the reference API, kernels.py:336-384,
+ * stream.py:260-316): copies the nseg host chunks (h_chunks[s], h_sizes[s] bytes, any
+ * host memory) into d_stage at 16-byte aligned offsets, runs hs_histogram_batched with
+ * d_ws, copies d_out[nseg][256] into h_out and waits for the stream. Everything else as
+ * hs_histogram_batched. d_stage must hold the chunks rounded up to 16 bytes each
+ * (HS_ERR_WORKSPACE otherwise). One call instead of a copy, a launch and a readback
+ * issued from Python: a 1 MiB image costs about half. Blocking. */
+int hs_histogram_host(const uint8_t* const* h_chunks, const uint64_t* h_sizes, int nseg, int kind, int impl,
+                      const int64_t* h_offset, const int64_t* h_count, int64_t total_slots, int64_t cap,
+                      uint8_t* d_stage, size_t stage_bytes, uint64_t* d_out, uint64_t* h_out,
+                      void* d_ws, size_t ws_bytes, void* stream);
+
 /* Single histogram: hs_histogram_batched with one segment [0, n_bytes).
  * Replaces naive_histogram (kernels.py:336-346) and adaptive_histogram
  * (kernels.py:349-384); `compute_histogram` (kernels.py:499-512) is the kind switch. */

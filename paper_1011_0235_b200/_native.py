@@ -62,6 +62,8 @@ EXPORTED = (
     "hs_validate_pattern",
     "hs_workspace_bytes",
     "hs_histogram_batched",
+    "hs_histogram_host",
+    "hs_histogram_sync",
     "hs_histogram",
     "hs_group_slots",
     "hs_ablation_stage",
@@ -90,6 +92,15 @@ _SIGNATURES = {
     "hs_histogram_batched": (
         _c.c_int,
         [_P, _U64P, _U64P, _c.c_int, _c.c_int, _c.c_int, _I64P, _I64P, _I64, _I64, _P, _P, _c.c_size_t, _P],
+    ),
+    "hs_histogram_sync": (
+        _c.c_int,
+        [_P, _U64P, _U64P, _c.c_int, _c.c_int, _c.c_int, _I64P, _I64P, _I64, _I64, _P, _U64P, _P, _c.c_size_t, _P],
+    ),
+    "hs_histogram_host": (
+        _c.c_int,
+        [_c.POINTER(_c.c_void_p), _U64P, _c.c_int, _c.c_int, _c.c_int, _I64P, _I64P, _I64, _I64, _P,
+         _c.c_size_t, _P, _U64P, _P, _c.c_size_t, _P],
     ),
     "hs_histogram": (
         _c.c_int,

@@ -28,6 +28,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <algorithm>
+#include <vector>
 
 #include "../../include/hist256.h"
 
@@ -1237,6 +1238,50 @@ int hs_histogram_batched(const uint8_t* d_data, const uint64_t* h_begin, const u
     if (rc != HS_OK) return rc;
   }
   return HS_OK;
+}
+
+int hs_histogram_sync(const uint8_t* d_data, const uint64_t* h_begin, const uint64_t* h_end, int nseg,
+                      int kind, int impl, const int64_t* h_offset, const int64_t* h_count,
+                      int64_t total_slots, int64_t cap, uint64_t* d_out, uint64_t* h_out,
+                      void* d_ws, size_t ws_bytes, void* stream) {
+  if (nseg > 0 && !h_out) return HS_ERR_INVALID_ARG;
+  int rc = hs_histogram_batched(d_data, h_begin, h_end, nseg, kind, impl, h_offset, h_count, total_slots, cap,
+                                d_out, d_ws, ws_bytes, stream);
+  if (rc != HS_OK || nseg == 0) return rc;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemcpyAsync(h_out, d_out, size_t(nseg) * 256 * sizeof(uint64_t), cudaMemcpyDeviceToHost, st);
+  if (e != cudaSuccess) return fold(e);
+  return fold(cudaStreamSynchronize(st));
+}
+
+int hs_histogram_host(const uint8_t* const* h_chunks, const uint64_t* h_sizes, int nseg, int kind, int impl,
+                      const int64_t* h_offset, const int64_t* h_count, int64_t total_slots, int64_t cap,
+                      uint8_t* d_stage, size_t stage_bytes, uint64_t* d_out, uint64_t* h_out,
+                      void* d_ws, size_t ws_bytes, void* stream) {
+  if (nseg < 0 || (nseg > 0 && (!h_chunks || !h_sizes || !d_out || !h_out))) return HS_ERR_INVALID_ARG;
+  if (nseg == 0) return HS_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  std::vector<uint64_t> begin(nseg), end(nseg);
+  uint64_t off = 0;
+  for (int s = 0; s < nseg; ++s) {
+    if (h_sizes[s] & 3) return HS_ERR_ALIGNMENT;
+    begin[s] = off;
+    end[s] = off + h_sizes[s];
+    off += (h_sizes[s] + 15) & ~uint64_t(15);
+  }
+  if (off > 0 && (!d_stage || stage_bytes < off)) return HS_ERR_WORKSPACE;
+  for (int s = 0; s < nseg; ++s) {
+    if (h_sizes[s] == 0) continue;
+    if (!h_chunks[s]) return HS_ERR_INVALID_ARG;
+    cudaError_t e = cudaMemcpyAsync(d_stage + begin[s], h_chunks[s], h_sizes[s], cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return fold(e);
+  }
+  int rc = hs_histogram_batched(d_stage, begin.data(), end.data(), nseg, kind, impl, h_offset, h_count, total_slots,
+                                cap, d_out, d_ws, ws_bytes, stream);
+  if (rc != HS_OK) return rc;
+  cudaError_t e = cudaMemcpyAsync(h_out, d_out, size_t(nseg) * 256 * sizeof(uint64_t), cudaMemcpyDeviceToHost, st);
+  if (e != cudaSuccess) return fold(e);
+  return fold(cudaStreamSynchronize(st));
 }
 
 int hs_histogram(const uint8_t* d_data, uint64_t n_bytes, int kind, int impl, const int64_t* h_offset,

@@ -42,11 +42,19 @@ class DeviceUnavailable(RuntimeError):
     """No CUDA device: the histogram path runs only on the GPU (no CPU fallback)."""
 
 
+_cuda_ok = False
+
+
 def require_cuda():
+    """torch, once a CUDA device and libhist256 are known to be there (checked on the
+    first call; later calls are on the per-image latency path and skip the probe)."""
+    global _cuda_ok
     t = torch()
-    if not t.cuda.is_available():
-        raise DeviceUnavailable("CUDA device required: libhist256 has no CPU fallback")
-    N.lib()
+    if not _cuda_ok:
+        if not t.cuda.is_available():
+            raise DeviceUnavailable("CUDA device required: libhist256 has no CPU fallback")
+        N.lib()
+        _cuda_ok = True
     return t
 
 
@@ -115,6 +123,7 @@ class Staging:
         self.device = t.device("cuda", t.cuda.current_device() if device is None else t.device(device).index)
         self._dev = None
         self._out_host = None
+        self._out_dev = None
         self._ws = None
 
     def device_bytes(self, n: int):
@@ -134,6 +143,13 @@ class Staging:
             n = int(N.lib().hs_workspace_bytes(64))
             self._ws = t.zeros(max(n, 256), dtype=t.uint8, device=self.device)
         return self._ws
+
+    def device_out(self, nseg: int):
+        """Device int64 [nseg, 256] counts buffer for the synchronous host path."""
+        t = torch()
+        if self._out_dev is None or self._out_dev.shape[0] < nseg:
+            self._out_dev = t.empty((max(nseg, 64), BINS), dtype=t.int64, device=self.device)
+        return self._out_dev[:nseg]
 
     def host_out(self, nseg: int):
         t = torch()
@@ -233,6 +249,13 @@ def _pattern_args(pattern):
 SPREAD_BELOW = 0.999
 
 
+def _with_hints(kind: int, pattern) -> int:
+    dom = getattr(pattern, "dominance", None)
+    if kind == N.HS_KIND_ADAPTIVE and dom is not None and dom < SPREAD_BELOW:
+        kind |= N.HS_KIND_FLAG_SPREAD
+    return kind
+
+
 def launch(staged: StagedBatch, kind: int, pattern=None, stream=None, impl: int = N.HS_IMPL_AUTO, out=None,
            staging: Staging | None = None):
     """hs_histogram_batched on ``stream`` (waits for the staging copies first): one
@@ -248,9 +271,7 @@ def launch(staged: StagedBatch, kind: int, pattern=None, stream=None, impl: int 
         with t.cuda.stream(stream):
             out = t.empty((max(nseg, 1), BINS), dtype=t.int64, device=t.cuda.current_device())
     off_p, cnt_p, S, cap, keep = _pattern_args(pattern)
-    dom = getattr(pattern, "dominance", None)
-    if kind == N.HS_KIND_ADAPTIVE and dom is not None and dom < SPREAD_BELOW:
-        kind |= N.HS_KIND_FLAG_SPREAD
+    kind = _with_hints(kind, pattern)
     begin = np.ascontiguousarray(staged.begin, dtype=np.uint64)
     end = np.ascontiguousarray(staged.end, dtype=np.uint64)
     status = N.lib().hs_histogram_batched(
@@ -298,9 +319,55 @@ def histograms(chunks: Sequence, kind: int, pattern=None, impl: int = N.HS_IMPL_
     t = require_cuda()
     stream = t.cuda.current_stream()
     st = default_staging()
+    if chunks and all(type(c) is PackedChunk for c in chunks):
+        return _host_histograms(chunks, kind, pattern, impl, st, stream)
+    if chunks and all(type(c) is DeviceChunk for c in chunks):
+        staged = stage(chunks, st, stream)
+        return _sync_histograms(staged, kind, pattern, impl, st, stream)
     staged = stage(chunks, st, stream)
     out = launch(staged, kind, pattern, stream, impl, staging=st)
     return readback(out, st, stream)
+
+
+def _host_histograms(chunks, kind, pattern, impl, st: "Staging", stream) -> np.ndarray:
+    """All-host batches in one native call (hs_histogram_host): H2D of every chunk, one
+    launch, D2H of the counts and the wait, without a Python round trip in between."""
+    import ctypes
+
+    n = len(chunks)
+    ptrs = (ctypes.c_void_p * n)(*[c.words.ctypes.data if c.words.size else None for c in chunks])
+    sizes = np.array([c.byte_size for c in chunks], dtype=np.uint64)
+    need = int(((sizes + 15) // 16 * 16).sum())
+    dev = st.device_bytes(max(need, 16))
+    out_dev = st.device_out(n)
+    h_out = st.host_out(n)  # pinned: the D2H stays a DMA
+    ws = st.workspace()
+    off_p, cnt_p, S, cap, keep = _pattern_args(pattern)
+    status = N.lib().hs_histogram_host(ptrs, N.u64p(sizes), n, int(_with_hints(kind, pattern)), int(impl),
+                                       off_p, cnt_p, S, cap, dev.data_ptr(), dev.numel(), out_dev.data_ptr(),
+                                       ctypes.cast(h_out.data_ptr(), N._U64P), ws.data_ptr(), ws.numel(),
+                                       stream.cuda_stream)
+    N.check(status, "hs_histogram_host")
+    return h_out.numpy().reshape(n, BINS).view(np.uint64).copy()
+
+
+def _sync_histograms(staged: StagedBatch, kind, pattern, impl, st: "Staging", stream) -> np.ndarray:
+    """Device-resident batches in one native call (hs_histogram_sync)."""
+    import ctypes
+
+    n = staged.nseg
+    out_dev = st.device_out(n)
+    h_out = st.host_out(n)
+    ws = st.workspace()
+    off_p, cnt_p, S, cap, keep = _pattern_args(pattern)
+    begin = np.ascontiguousarray(staged.begin, dtype=np.uint64)
+    end = np.ascontiguousarray(staged.end, dtype=np.uint64)
+    status = N.lib().hs_histogram_sync(staged.base or None, N.u64p(begin), N.u64p(end), n,
+                                       int(_with_hints(kind, pattern)), int(impl), off_p, cnt_p, S, cap,
+                                       out_dev.data_ptr(), ctypes.cast(h_out.data_ptr(), N._U64P), ws.data_ptr(),
+                                       ws.numel(), stream.cuda_stream)
+    N.check(status, "hs_histogram_sync")
+    return h_out.numpy().reshape(n, BINS).view(np.uint64).copy()
 
 
 def histogram_tensor(data, kind: int = N.HS_KIND_NAIVE, pattern=None, impl: int = N.HS_IMPL_AUTO,
