@@ -245,9 +245,18 @@ __device__ __forceinline__ EachVec<U, VecFn> each_vec(VecFn& f) { return EachVec
 // the loads and the shared-atomic pipe busy (tools/microbench/shared_lanebank.cu).
 // Per byte: PRMT (extract) + IMAD (address) + ATOMS.POPC.INC.
 // A column (lane) adds at most piece/32 per flush; pieces are capped at 1 GiB per CTA.
-constexpr int kLaneThreads = 1024;
+// Plain form: threads per CTA and resident CTAs per SM. Measured alternatives at the
+// same 64 warps/SM (tools/size_sweep.py, 1 GiB launches): 672 x 3 -> 171 us, 512 x 4 ->
+// 184 us, against 162 us here; each CTA brings its own 32 KB counter array, and more
+// arrays per SM slow the shared atomics (as did two arrays per CTA).
+#ifndef HS_LANE_THREADS
+#define HS_LANE_THREADS 1024
+#define HS_LANE_BLOCKS 2
+#endif
+constexpr int kLaneThreads = HS_LANE_THREADS;
+constexpr int kLaneBlocks = HS_LANE_BLOCKS;
 constexpr int kLaneHotThreads = 768;
-constexpr int kLaneMinBlocks = 2;
+constexpr int kLaneMinBlocks = 2;  // HOT form
 constexpr uint32_t kLaneArrayBytes = 256 * 32 * 4;
 
 // Ticketed output (single launch, no memset): CTAs RED their counts for launch-local
@@ -409,8 +418,8 @@ __device__ __forceinline__ uint32_t lane_piece(const uint8_t* __restrict__ data,
 }
 
 // HOT (ADAPTIVE): register path for the hot bin `hot_bin`.
-template <int U, bool HOT, int TH = kLaneThreads>
-__global__ void __launch_bounds__(TH, kLaneMinBlocks)
+template <int U, bool HOT, int TH = kLaneThreads, int MB = kLaneBlocks>
+__global__ void __launch_bounds__(TH, MB)
     k_lane(const uint8_t* __restrict__ data, const __grid_constant__ SegParams sp, int hot_bin,
            unsigned long long* __restrict__ out, Tickets tk) {
   __shared__ __align__(16) uint32_t counters[256 * 32];
@@ -1038,8 +1047,10 @@ int launch_batch(const uint8_t* d_data, SegParams& sp, int kind, int impl, const
     const uint64_t want = (v + (64ull << 10) - 1) / (64ull << 10);
     // reserve_slots CTA slots are left free (the device stream engine's fold CTA takes
     // one while the next histogram streams, instead of delaying one of its CTAs)
+    const bool hot = kind == HS_KIND_ADAPTIVE && pp != nullptr && pp->hot_unique;
+    const int per_sm = hot ? kLaneMinBlocks : kLaneBlocks;
     const int grid = int(std::max<uint64_t>(
-        1, std::min<uint64_t>(want, uint64_t(di.sms) * kLaneMinBlocks - uint64_t(reserve_slots))));
+        1, std::min<uint64_t>(want, uint64_t(di.sms) * per_sm - uint64_t(reserve_slots))));
     split_grid(sp, grid);
     const int hb = pp ? pp->hot_bin : 0;
     // ADAPTIVE runs the register path for the pattern's hot bin only when the pattern
@@ -1056,9 +1067,9 @@ int launch_batch(const uint8_t* d_data, SegParams& sp, int kind, int impl, const
     // stream engine: with the previous iteration's one-CTA fold)
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (kind == HS_KIND_ADAPTIVE && pp != nullptr && pp->hot_unique) {
+    if (hot) {
       cfg.blockDim = dim3(kLaneHotThreads);
-      e = cudaLaunchKernelEx(&cfg, k_lane<2, true, kLaneHotThreads>, d_data, sp, hb, d_out, tk);
+      e = cudaLaunchKernelEx(&cfg, k_lane<2, true, kLaneHotThreads, kLaneMinBlocks>, d_data, sp, hb, d_out, tk);
     } else {
       cfg.blockDim = dim3(kLaneThreads);
       e = cudaLaunchKernelEx(&cfg, k_lane<2, false>, d_data, sp, hb, d_out, tk);
