@@ -14,6 +14,7 @@ DeviceChunks skip the H2D: their tensors are segments of the same launch.
 from __future__ import annotations
 
 import bisect
+import ctypes
 import threading
 import warnings
 import weakref
@@ -206,18 +207,32 @@ def stage(chunks: Sequence, staging: Staging | None, stream=None) -> StagedBatch
         keep.append(dev)
         base = dev.data_ptr()
         off = 0
+        # chunks that sit back to back in host memory (slices of one pinned stream) go
+        # in one copy: 16 MiB copies reach 54.5 GB/s, 128 MiB ones 55.2 GB/s
+        runs: list[list] = []  # [host_ptr, dev_off, nbytes, first chunk array]
+        for i, c in host:
+            n = c.byte_size
+            ptrs[i] = base + off
+            sizes[i] = n
+            if n:
+                hp = c.words.ctypes.data
+                if runs and runs[-1][0] + runs[-1][2] == hp and runs[-1][1] + runs[-1][2] == off:
+                    runs[-1][2] += n
+                else:
+                    runs.append([hp, off, n, c.words])
+                keep.append(c.words)
+            off += n
         with t.cuda.stream(stream):
-            for i, c in host:
-                n = c.byte_size
-                if n:
-                    with warnings.catch_warnings():  # chunks are read-only views; torch only reads them
-                        warnings.simplefilter("ignore", UserWarning)
-                        src = t.from_numpy(c.words.view(np.uint8))
-                    dev[off:off + n].copy_(src, non_blocking=True)
-                    keep.append(src)
-                ptrs[i] = base + off
-                sizes[i] = n
-                off += n
+            for hp, doff, n, first in runs:
+                if n == first.nbytes:
+                    arr = first.view(np.uint8)
+                else:  # the run spans several chunks' memory (all kept alive above)
+                    arr = np.ctypeslib.as_array((ctypes.c_uint8 * n).from_address(hp))
+                with warnings.catch_warnings():  # chunks are read-only views; torch only reads them
+                    warnings.simplefilter("ignore", UserWarning)
+                    src = t.from_numpy(arr)
+                dev[doff:doff + n].copy_(src, non_blocking=True)
+                keep.append(src)
             ready = t.cuda.Event()
             ready.record(stream)
     for i, c in enumerate(chunks):
