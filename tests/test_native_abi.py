@@ -133,3 +133,28 @@ def test_streaming_loop_sass_is_clean():
         assert r["local"] == 0 and r["r2ur"] == 0, r
     # per 16 B x 4 vectors x 4 bytes: PRMT + address + ATOMS, plus loads and loop control
     assert all(r["len"] <= 210 for r in main if "Lb0" in r["kernel"]), main
+
+
+def test_sync_entry_points_validate_first():
+    """hs_histogram_host / hs_histogram_sync reject bad arguments before any copy."""
+    lib = N.lib()
+    host = np.zeros(64, np.uint8)
+    ptrs = (ctypes.c_void_p * 1)(host.ctypes.data)
+    p = ctypes.c_void_p(256)  # never dereferenced: validation fails first
+    h_out = np.zeros((1, 256), np.uint64)
+    bad = np.array([6], np.uint64)  # not a word multiple
+    assert lib.hs_histogram_host(ptrs, N.u64p(bad), 1, 0, 0, None, None, 0, 0, p, 1 << 20, p, N.u64p(h_out),
+                                 None, 0, None) == N.HS_ERR_ALIGNMENT
+    sizes = np.array([64], np.uint64)
+    assert lib.hs_histogram_host(ptrs, N.u64p(sizes), 1, 0, 0, None, None, 0, 0, p, 32, p, N.u64p(h_out),
+                                 None, 0, None) == N.HS_ERR_WORKSPACE
+    assert lib.hs_histogram_host(ptrs, N.u64p(sizes), 1, 0, 0, None, None, 0, 0, p, 64, p, None,
+                                 None, 0, None) == N.HS_ERR_INVALID_ARG
+    assert lib.hs_histogram_host(ptrs, N.u64p(sizes), 0, 0, 0, None, None, 0, 0, None, 0, None, None,
+                                 None, 0, None) == N.HS_OK
+    b = np.zeros(1, np.uint64)
+    e = np.full(1, 8, np.uint64)
+    assert lib.hs_histogram_sync(p, N.u64p(b), N.u64p(e), 1, 0, 0, None, None, 0, 0, p, None, None, 0,
+                                 None) == N.HS_ERR_INVALID_ARG
+    assert lib.hs_histogram_sync(p, N.u64p(b), N.u64p(e), 1, 7, 0, None, None, 0, 0, p, N.u64p(h_out), None, 0,
+                                 None) == N.HS_ERR_INVALID_ARG
