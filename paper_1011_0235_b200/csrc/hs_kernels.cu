@@ -423,12 +423,28 @@ __global__ void __launch_bounds__(TH, MB)
     k_lane(const uint8_t* __restrict__ data, const __grid_constant__ SegParams sp, int hot_bin,
            unsigned long long* __restrict__ out, Tickets tk) {
   __shared__ __align__(16) uint32_t counters[256 * 32];
+  // The CTA's pieces (segment, byte range) are listed in shared memory first, so no
+  // segment-walk state is live across the streaming loop (it would take registers the
+  // loop needs at 64 resident warps).
+  __shared__ uint64_t pc_p0[kMaxSeg], pc_p1[kMaxSeg];
+  __shared__ int pc_seg[kMaxSeg];
+  __shared__ int pc_n;
   HS_STAMP(0);
+  pdl_launch_dependents();  // the next launch's CTAs may take SMs as ours retire
+  if (threadIdx.x == 0) {
+    int n = 0;
+    for_each_piece<~0ull>(sp, [&](int s, uint64_t p0, uint64_t p1) {
+      pc_p0[n] = p0;
+      pc_p1[n] = p1;
+      pc_seg[n] = s;
+      ++n;
+    });
+    pc_n = n;
+  }
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(counters);
   for (uint32_t i = threadIdx.x; i < kLaneArrayBytes / 16; i += blockDim.x) sh_st4(sbase + i * 16, make_uint4(0, 0, 0, 0));
   __syncthreads();
   const uint32_t tb = sbase + (threadIdx.x & 31) * 4;  // column base: bank == lane
-  pdl_launch_dependents();  // the next launch's CTAs may take SMs as ours retire
   const uint32_t hot = uint32_t(hot_bin) & 0xff;
   if (tk.ticket != nullptr && blockIdx.x == 0) {
     // ticketed launches have no memset: CTA 0 zeroes the empty segments' outputs
@@ -444,23 +460,6 @@ __global__ void __launch_bounds__(TH, MB)
   // u32 columns: a column adds at most (CTA bytes)/32 <= 2^32, so one flush per
   // (CTA, segment) suffices -- required by the ticketed output
   const uint32_t hot4 = hot * 0x01010101u;
-  // The CTA's pieces (segment, byte range) are listed in shared memory first, so no
-  // segment-walk state is live across the streaming loop (it would take registers the
-  // loop needs at 64 resident warps).
-  __shared__ uint64_t pc_p0[kMaxSeg], pc_p1[kMaxSeg];
-  __shared__ int pc_seg[kMaxSeg];
-  __shared__ int pc_n;
-  if (threadIdx.x == 0) {
-    int n = 0;
-    for_each_piece<~0ull>(sp, [&](int s, uint64_t p0, uint64_t p1) {
-      pc_p0[n] = p0;
-      pc_p1[n] = p1;
-      pc_seg[n] = s;
-      ++n;
-    });
-    pc_n = n;
-  }
-  __syncthreads();
   const bool ticketed = tk.ticket != nullptr;
   HS_STAMP(1);
   for (int i = 0; i < pc_n; ++i) {
