@@ -28,6 +28,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <algorithm>
+#include <atomic>
 #include <vector>
 
 #include "../../include/hist256.h"
@@ -1015,6 +1016,19 @@ int set_smem(K kernel, size_t bytes) {
   return fold(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
 }
 
+// set_smem once per device (the attribute belongs to the current device's context):
+// `done` is a per-kernel bitmask of devices already configured
+template <class K>
+int set_smem_once(K kernel, size_t bytes, std::atomic<uint64_t>& done) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return set_smem(kernel, bytes);
+  const uint64_t bit = 1ull << dev;
+  if (done.load(std::memory_order_acquire) & bit) return HS_OK;
+  const int rc = set_smem(kernel, bytes);
+  if (rc == HS_OK) done.fetch_or(bit, std::memory_order_acq_rel);
+  return rc;
+}
+
 // CTA index owning word w of the balanced split of tw words over g CTAs
 uint32_t cta_of_word(uint64_t w, uint64_t tw, uint64_t g) {
   const uint64_t q = tw / g, r = tw % g;
@@ -1196,7 +1210,6 @@ int hs_histogram_batched(const uint8_t* d_data, const uint64_t* h_begin, const u
                          int kind, int impl, const int64_t* h_offset, const int64_t* h_count,
                          int64_t total_slots, int64_t cap, uint64_t* d_out, void* d_ws, size_t ws_bytes,
                          void* stream) {
-  (void)d_ws; (void)ws_bytes;
   if (nseg < 0 || (nseg > 0 && (!h_begin || !h_end || !d_out))) return HS_ERR_INVALID_ARG;
   const bool spread = (kind & HS_KIND_FLAG_SPREAD) != 0;
   kind &= ~HS_KIND_FLAG_SPREAD;
@@ -1423,8 +1436,8 @@ int hs_stream_step(const uint8_t* d_data, const uint64_t* h_begin, const uint64_
   }
   // pattern and kernel refresh for iteration+1 when (iteration+1) % every == 0 (stream.py:407-414)
   const int decide = ((iteration + 1) % recompute_every) == 0;
-  static const int rc_fold = set_smem(k_stream_fold, kFoldSmem);
-  if (rc_fold != HS_OK) return rc_fold;
+  static std::atomic<uint64_t> fold_smem_set{0};
+  if ((rc = set_smem_once(k_stream_fold, kFoldSmem, fold_smem_set)) != HS_OK) return rc;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(1);
   cfg.blockDim = dim3(kFoldThreads);

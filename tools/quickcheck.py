@@ -1,9 +1,7 @@
 """Quick on-GPU check of libhist256: correctness of every impl vs torch.bincount and
 CUDA-event throughput. Development tool (not the bench, not a test)."""
-import ctypes
 import os
 import sys
-import time
 
 import numpy as np
 import torch

@@ -1,7 +1,6 @@
 """Copy/compute overlap of the host-streamed pipeline (BASELINE configs[3] shape):
 pinned 16 MiB chunks, batches of 4, run_pipeline on a copy and a compute stream.
 Writes profiles/<tag>_stream_timeline.csv and prints the overlap summary."""
-import os
 import sys
 from pathlib import Path
 
