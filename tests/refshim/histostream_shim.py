@@ -9,7 +9,7 @@ import sys
 import paper_1011_0235_b200 as pkg
 
 sys.modules["histostream"] = pkg
-for _name in ("core", "datagen", "kernels", "pattern", "policy", "stream", "cli"):
+for _name in ("bench", "core", "datagen", "kernels", "pattern", "policy", "stream", "cli"):
     sys.modules[f"histostream.{_name}"] = importlib.import_module(f"paper_1011_0235_b200.{_name}")
 
 try:

@@ -261,3 +261,33 @@ def test_pattern_dominance_hint():
     assert hs.uniform_pattern(960).dominance is None
     q = hs.BinningPattern(p.offset, p.count, p.total_slots, p.cap)
     assert q == p and q.dominance is None
+
+
+def test_bench_helpers():
+    """histostream.bench restated: median, interquartile spread, guarded ordering; equal
+    to the reference module's values when the reference checkout is present."""
+    import importlib.util
+    import random
+    from pathlib import Path
+
+    from paper_1011_0235_b200 import bench as B
+
+    assert B.median([3.0, 1.0, 2.0]) == 2.0 and B.median([4.0, 1.0, 2.0, 3.0]) == 2.5
+    assert B.relative_spread([1.0]) == 0.0
+    assert B.ordering(1.2, 1.0) is B.Verdict.CONFIRMED
+    assert B.ordering(1.0, 1.2) is B.Verdict.INVERTED
+    assert B.ordering(1.05, 1.0) is B.Verdict.INCONCLUSIVE
+    calls = []
+    s = B.interleaved_samples({"a": lambda: calls.append("a"), "b": lambda: calls.append("b")}, 3, shuffle_seed=1)
+    assert len(s["a"]) == 3 and len(s["b"]) == 3 and len(calls) == 8
+    ref = Path("/root/reference/pkg/src/histostream/bench.py")
+    if ref.exists():
+        spec = importlib.util.spec_from_file_location("ref_bench", ref)
+        R = importlib.util.module_from_spec(spec)
+        spec.loader.exec_module(R)
+        rng = random.Random(3)
+        for n in range(1, 40):
+            xs = [rng.random() for _ in range(n)]
+            assert B.median(xs) == R.median(xs) and B.relative_spread(xs) == R.relative_spread(xs), n
+        for a, b in ((1.0, 1.0), (1.11, 1.0), (1.0, 1.11), (2.0, 1.0)):
+            assert B.ordering(a, b).value == R.ordering(a, b).value
