@@ -65,7 +65,10 @@ def host_cores() -> int:
 
 # ----------------------------------------------------------------------- clocks
 class ClockSampler:
-    """NVML SM clock + throttle reasons sampled every 5 ms during the timed region."""
+    """NVML SM clock, memory clock, power and clock-event reasons, sampled every ~5 ms by
+    a thread started ahead of the timed region (its first NVML calls can be slow right
+    after an idle period); the summary keeps the samples taken inside the window that
+    mark_start()/mark_end() bracket."""
 
     BAD = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20}
     NAMES = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
@@ -73,11 +76,9 @@ class ClockSampler:
              0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
 
     def __init__(self, index: int):
-        self.samples: list[int] = []
-        self.mem_samples: list[int] = []
-        self.power: list[float] = []
-        self.reasons = 0
+        self.rows: list[tuple] = []  # (t, sm_mhz, mem_mhz, power_w, reasons)
         self.max_mhz = None
+        self.t0 = self.t1 = None
         self._stop = threading.Event()
         try:
             import pynvml
@@ -90,12 +91,12 @@ class ClockSampler:
             self.nv = None
 
     def _run(self):
+        nv, h = self.nv, self.h
         while not self._stop.is_set():
             try:
-                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
-                self.mem_samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_MEM))
-                self.power.append(self.nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0)
-                self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.rows.append((time.perf_counter(), nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM),
+                                  nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_MEM), nv.nvmlDeviceGetPowerUsage(h) / 1000.0,
+                                  nv.nvmlDeviceGetCurrentClocksEventReasons(h)))
             except Exception:
                 pass
             time.sleep(0.005)
@@ -108,19 +109,35 @@ class ClockSampler:
             self._t.start()
         return self
 
+    def mark_start(self):
+        self.t0 = time.perf_counter()
+
+    def mark_end(self):
+        self.t1 = time.perf_counter()
+
     def __exit__(self, *exc):
         self._stop.set()
         if self.nv is not None:
             self._t.join()
 
     def summary(self):
-        if self.nv is None or not self.samples:
+        if self.nv is None or not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
-        reasons = [n for bit, n in self.NAMES.items() if self.reasons & bit and bit != 0x1]
-        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
-                "reasons": reasons, "samples": len(self.samples),
-                "mem_mhz": float(statistics.median(self.mem_samples)) if self.mem_samples else None,
-                "power_w_max": round(max(self.power), 1) if self.power else None}
+        t0 = self.t0 if self.t0 is not None else self.rows[0][0]
+        t1 = self.t1 if self.t1 is not None else self.rows[-1][0]
+        inside = [r for r in self.rows if t0 <= r[0] <= t1]
+        if not inside:  # a sample could not be taken inside: the nearest one on each side
+            before = [r for r in self.rows if r[0] < t0]
+            after = [r for r in self.rows if r[0] > t1]
+            inside = before[-1:] + after[:1]
+        bits = 0
+        for r in inside:
+            bits |= r[4]
+        reasons = [n for bit, n in self.NAMES.items() if bits & bit and bit != 0x1]
+        return {"sm_mhz": float(statistics.median(r[1] for r in inside)), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(inside),
+                "mem_mhz": float(statistics.median(r[2] for r in inside)),
+                "power_w_max": round(max(r[3] for r in inside), 1)}
 
 
 # ----------------------------------------------------------------------- distributed
@@ -375,12 +392,14 @@ def main(argv=None):
     # The timed region starts from an idle GPU: this kernel draws the board's 1000 W
     # limit within ~50 ms, so whatever ran just before would otherwise decide how much
     # of the region runs power-capped. The capped rate is reported as `sustained`.
+    clocks = ClockSampler(local).__enter__()  # running before the settle: see the class
     time.sleep(args.settle_seconds)
     barrier(world)
     torch.cuda.synchronize()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clocks:
+    try:
+        clocks.mark_start()
         t0.record(stream)
         for sj in side:
             sj.wait_stream(stream)
@@ -395,6 +414,9 @@ def main(argv=None):
         stream.wait_stream(red_stream)
         t1.record(stream)
         torch.cuda.synchronize()
+        clocks.mark_end()
+    finally:
+        clocks.__exit__(None, None, None)
     barrier(world)
     elapsed_ms = max_over_ranks(t0.elapsed_time(t1), world)
     if os.environ.get("HS_BENCH_DEBUG"):
@@ -420,6 +442,7 @@ def main(argv=None):
         torch.cuda.synchronize()
         s0e, s1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with ClockSampler(local) as sus_clocks:
+            sus_clocks.mark_start()
             s0e.record(stream)
             for sj in side:
                 sj.wait_stream(stream)
@@ -430,6 +453,7 @@ def main(argv=None):
             stream.wait_stream(red_stream)
             s1e.record(stream)
             torch.cuda.synchronize()
+            sus_clocks.mark_end()
         sus_ms = max_over_ranks(s0e.elapsed_time(s1e), world)
         sustained = {"steps": n_sus, "seconds": round(sus_ms / 1e3, 3),
                      "value": round(world * bytes_per_step_rank * n_sus / (sus_ms / 1e3) / 1e9, 2), "unit": "GB/s",
