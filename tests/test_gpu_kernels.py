@@ -346,3 +346,45 @@ def test_register_path_on_partially_hot_data(cuda, oracle, p):
     assert (prior.dominance >= D.SPREAD_BELOW) == (p >= 0.999)
     got = hs.adaptive_histogram(hs.DeviceChunk(buf), prior, hs.WorkerGroupConfig())
     assert got.counts.tolist() == want.tolist()
+
+
+def test_graph_replay_ticketed(cuda, oracle):
+    """Ticketed launches captured into a CUDA graph (programmatic edges between them)
+    give the same counts on every replay: each launch leaves its workspace zeroed."""
+    torch = cuda
+    n = (48 << 20) + 12
+    host = oracle.generate("normal", n, 5, mean=100.0, sigma=20.0)
+    buf = torch.from_numpy(host.copy()).cuda()
+    want = oracle.histogram(host)
+    L = N.lib()
+    b0 = np.array([0, 4096, 12 << 20], np.uint64)
+    b1 = np.array([4096, 12 << 20, n], np.uint64)
+    parts = [oracle.histogram(host[int(a):int(b)]) for a, b in zip(b0, b1)]
+    assert (sum(parts) == want).all()
+    ws = torch.zeros(int(L.hs_workspace_bytes(64)), dtype=torch.uint8, device="cuda")
+    outs = [torch.empty((3, 256), dtype=torch.int64, device="cuda") for _ in range(3)]
+    side = torch.cuda.Stream()
+
+    def enqueue():
+        s = torch.cuda.current_stream().cuda_stream
+        for o in outs:
+            N.check(L.hs_histogram_batched(buf.data_ptr(), N.u64p(b0), N.u64p(b1), 3, N.HS_KIND_NAIVE,
+                                           N.HS_IMPL_LANE, None, None, 0, 0, o.data_ptr(), ws.data_ptr(),
+                                           ws.numel(), s), "graph")
+
+    with torch.cuda.stream(side):
+        enqueue()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=side):
+        enqueue()
+    for _ in range(3):
+        for o in outs:
+            o.fill_(-1)
+        g.replay()
+        torch.cuda.synchronize()
+        for o in outs:
+            got = o.cpu().numpy().view(np.uint64)
+            for k in range(3):
+                assert got[k].tolist() == parts[k].tolist()
+    assert not ws.any().item()
