@@ -522,10 +522,14 @@ def main(argv=None):
     return 0
 
 
+C1_IMAGES = 256
+
+
 def c1_image(hs, N, torch, L, dev):
     """BASELINE configs[0]: one 1024x1024 uniform image (seed 0). L2-resident and
     launch-bound, so reported beside the headline: latency through the public API,
-    64 images per launch, and single-image launches replayed from a CUDA graph."""
+    256 images per call (one launch of 256 segments), and single-image launches
+    replayed from a CUDA graph."""
     from oracle import oracle as O
 
     n = 1 << 20
@@ -540,19 +544,19 @@ def c1_image(hs, N, torch, L, dev):
     for _ in range(50):
         hs.naive_histogram(chunk, cfg)
     api_us = (time.perf_counter() - t0) / 50 * 1e6
-    # 64 images, one launch
-    imgs = torch.empty(64 * n, dtype=torch.uint8, device=dev)
-    for i in range(64):
+    # C1_IMAGES images, one call
+    imgs = torch.empty(C1_IMAGES * n, dtype=torch.uint8, device=dev)
+    for i in range(C1_IMAGES):
         hs.generate_device(hs.SourceSpec("uniform", n, i), imgs[i * n:(i + 1) * n])
-    b0 = (np.arange(64, dtype=np.uint64) * n)
+    b0 = (np.arange(C1_IMAGES, dtype=np.uint64) * n)
     b1 = b0 + n
-    out = torch.empty((64, 256), dtype=torch.int64, device=dev)
-    ws = torch.zeros(int(L.hs_workspace_bytes(64)), dtype=torch.uint8, device=dev)
+    out = torch.empty((C1_IMAGES, 256), dtype=torch.int64, device=dev)
+    ws = torch.zeros(int(L.hs_workspace_bytes(C1_IMAGES)), dtype=torch.uint8, device=dev)
     s = torch.cuda.current_stream()
 
     def batched():
-        N.check(L.hs_histogram_batched(imgs.data_ptr(), N.u64p(b0), N.u64p(b1), 64, N.HS_KIND_NAIVE, 0, None, None,
-                                       0, 0, out.data_ptr(), ws.data_ptr(), ws.numel(), s.cuda_stream), "batched")
+        N.check(L.hs_histogram_batched(imgs.data_ptr(), N.u64p(b0), N.u64p(b1), C1_IMAGES, N.HS_KIND_NAIVE, 0, None,
+                                       None, 0, 0, out.data_ptr(), ws.data_ptr(), ws.numel(), s.cuda_stream), "batched")
 
     for _ in range(3):
         batched()
@@ -564,6 +568,8 @@ def c1_image(hs, N, torch, L, dev):
     b.record()
     b.synchronize()
     batch_us = a.elapsed_time(b) / 20 * 1e3
+    assert np.array_equal(out[C1_IMAGES - 1].cpu().numpy().view(np.uint64),
+                          O.histogram(imgs[(C1_IMAGES - 1) * n:].cpu().numpy()))
     # single-image launches captured in a CUDA graph
     one0, one1 = np.zeros(1, np.uint64), np.full(1, n, np.uint64)
     out1 = torch.empty((1, 256), dtype=torch.int64, device=dev)
@@ -593,8 +599,8 @@ def c1_image(hs, N, torch, L, dev):
         O.naive_histogram(chunk.words, 32, host_cores())
     cpu_us = (time.perf_counter() - t0) / 5 * 1e6
     return {"bytes": n, "public_api_us_per_image": round(api_us, 2),
-            "batched_64_images_us_per_image": round(batch_us / 64, 3),
-            "batched_64_images_gbs": round(64 * n / (batch_us * 1e3), 1),
+            "batched_images": C1_IMAGES, "batched_us_per_image": round(batch_us / C1_IMAGES, 3),
+            "batched_gbs": round(C1_IMAGES * n / (batch_us * 1e3), 1),
             "graph_single_image_us": round(graph_us, 3), "cpu_reference_port_us": round(cpu_us, 1)}
 
 

@@ -80,7 +80,10 @@ int hs_device_query(int device, int* sm_count, int* smem_optin, int* l2_bytes);
 int hs_validate_pattern(const int64_t* h_offset, const int64_t* h_count,
                         int64_t total_slots, int64_t cap);
 
-/* Device workspace of hs_histogram_batched / hs_stream_step (tickets + accumulator rows). */
+/* Device workspace of hs_histogram_batched / hs_stream_step: 1 KB of tickets plus one
+ * 2 KB accumulator row per segment of a launch, for launches of up to nseg segments
+ * (clamped to [64, 256]). A workspace sized for n segments makes the call launch groups
+ * of n segments; hs_stream_step needs at least hs_workspace_bytes(64). */
 size_t hs_workspace_bytes(int nseg);
 
 /*

@@ -35,7 +35,9 @@
 
 namespace {
 
-constexpr int kMaxSeg = 64;
+constexpr int kMaxSeg = 256;         // segments per launch (SegParams ~5 KB: large kernel params)
+constexpr int kMaxSegEngine = 64;    // per hs_stream_step batch (the fold stages it in shared memory)
+constexpr size_t kTicketBytes = 1024;  // workspace head: kMaxSeg u32 tickets
 constexpr uint64_t kBigCap = 1ull << 30;  // u32 per-warp counters: far from wrapping
 
 struct SegParams {
@@ -46,7 +48,7 @@ struct SegParams {
   int acc_base;                  // its workspace accumulator row / ticket index
   // segments that continue in the next launch of the same call (bit s): their CTAs
   // only RED into the accumulator row; the launch holding a segment's end finalizes it
-  unsigned long long open_mask;
+  uint32_t open_mask[kMaxSeg / 32];
   // balanced split of the concatenated words over the grid, precomputed on the host
   // (no 64-bit division on the device): CTA b owns q words, plus one if b < r
   uint64_t q, r;
@@ -305,25 +307,25 @@ __device__ __forceinline__ void lane_flush(uint32_t sbase, unsigned long long* _
 // the ticket, so workspace and tickets are zero again when the launch ends.
 __device__ __forceinline__ void lane_tickets(const Tickets& tk, const SegParams& sp, int s_first, int s_last,
                                           unsigned long long* __restrict__ out) {
-  __shared__ unsigned long long lastmask;
+  __shared__ int last_seg[kMaxSeg];
+  __shared__ int n_last;
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
-    unsigned long long m = 0;
+    int m = 0;
     for (int s = s_first; s <= s_last; ++s) {
       if (sp.vstart[s + 1] == sp.vstart[s]) continue;  // empty: no CTA owns it
-      if ((sp.open_mask >> s) & 1) continue;            // finalized by a later launch
-      if (atomicAdd(tk.ticket + sp.acc_base + s, 1u) == sp.ctas_after_first[s]) m |= 1ull << s;
+      if ((sp.open_mask[s >> 5] >> (s & 31)) & 1) continue;  // finalized by a later launch
+      if (atomicAdd(tk.ticket + sp.acc_base + s, 1u) == sp.ctas_after_first[s]) last_seg[m++] = s;
     }
-    lastmask = m;
+    n_last = m;
   }
   __syncthreads();
-  unsigned long long m = lastmask;
+  const int m = n_last;
   if (m) {
     __threadfence();
-    while (m) {
-      const int s = __ffsll(m) - 1;
-      m &= m - 1;
+    for (int k = 0; k < m; ++k) {
+      const int s = last_seg[k];
       for (uint32_t b = threadIdx.x; b < 256; b += blockDim.x)
         out[size_t(sp.out_base + s) * 256 + b] = atomicExch(tk.acc + size_t(sp.acc_base + s) * 256 + b, 0ull);
       if (threadIdx.x == 0) tk.ticket[sp.acc_base + s] = 0;
@@ -748,7 +750,7 @@ constexpr int kFoldThreads = 256;  // one thread per bin; small enough to share 
                                    // with a histogram CTA of the next iteration
 constexpr int kFoldBatch = 8;      // pushes whose inputs are loaded per round (registers)
 constexpr int kFoldSmallWin = 16;  // windows below this keep the ring in shared memory
-constexpr size_t kFoldSmem = size_t(kMaxSeg) * 256 * 8 + size_t(kFoldSmallWin - 1) * 256 * 8;
+constexpr size_t kFoldSmem = size_t(kMaxSegEngine) * 256 * 8 + size_t(kFoldSmallWin - 1) * 256 * 8;
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
   unsigned long long t;
@@ -1135,7 +1137,7 @@ int launch_segments(const uint8_t* d_data, const uint64_t* h_begin, const uint64
     const bool last = v1 == total;
     SegParams sp;
     sp.nseg = 0;
-    sp.open_mask = 0;
+    for (auto& w : sp.open_mask) w = 0;
     sp.acc_base = -1;
     for (int i = 0; i < ns; ++i) {
       // a non-empty segment joins every launch it intersects; an empty one the launch
@@ -1149,7 +1151,7 @@ int launch_segments(const uint8_t* d_data, const uint64_t* h_begin, const uint64
       sp.begin[k] = h_begin[s0 + i] + (empty ? 0 : a - vs[i]);
       sp.vstart[k] = (empty ? std::min(vs[i], v1) : a) - v0;
       sp.vstart[k + 1] = (empty ? std::min(vs[i], v1) : b) - v0;
-      if (vs[i + 1] > v1) sp.open_mask |= 1ull << k;
+      if (vs[i + 1] > v1) sp.open_mask[k >> 5] |= 1u << (k & 31);
     }
     sp.out_base = s0 + sp.acc_base;
     int rc = launch_batch(d_data, sp, kind, impl, pp, d_out, st, di, tk, reserve_slots);
@@ -1201,10 +1203,14 @@ int hs_validate_pattern(const int64_t* h_offset, const int64_t* h_count, int64_t
   return validate(h_offset, h_count, total_slots, cap);
 }
 
-// [tickets: kMaxSeg u32, padded to 256 B][accumulators: kMaxSeg x 256 u64]; zero it once
-// after allocating -- every ticketed launch leaves it zero again.
-constexpr size_t kWorkspaceBytes = 256 + size_t(kMaxSeg) * 256 * sizeof(uint64_t);
-size_t hs_workspace_bytes(int nseg) { return nseg < 0 ? 0 : kWorkspaceBytes; }
+// [tickets: kMaxSeg u32 = 1 KB][accumulators: one 256 x u64 row per segment of a
+// launch]; zero it once after allocating -- every ticketed launch leaves it zero again.
+// A workspace sized for n segments lets launches take up to n (<= kMaxSeg) segments.
+constexpr size_t ws_bytes_for(int nseg) { return kTicketBytes + size_t(nseg) * 256 * sizeof(uint64_t); }
+constexpr size_t kWorkspaceBytes = ws_bytes_for(kMaxSegEngine);  // the minimum accepted
+size_t hs_workspace_bytes(int nseg) {
+  return nseg < 0 ? 0 : ws_bytes_for(std::max(kMaxSegEngine, std::min(nseg, kMaxSeg)));
+}
 
 int hs_histogram_batched(const uint8_t* d_data, const uint64_t* h_begin, const uint64_t* h_end, int nseg,
                          int kind, int impl, const int64_t* h_offset, const int64_t* h_count,
@@ -1237,18 +1243,21 @@ int hs_histogram_batched(const uint8_t* d_data, const uint64_t* h_begin, const u
   int rc = dev_info(di);
   if (rc != HS_OK) return rc;
   if (impl == HS_IMPL_AUTO) impl = HS_IMPL_LANE;
-  // LANE with a workspace: one launch per <= 64 segments, output written in-kernel
+  // LANE with a workspace: one launch per group of segments the workspace has rows for
+  // (<= kMaxSeg), output written in-kernel; otherwise memset + RED, kMaxSeg per launch
   Tickets tk{nullptr, nullptr};
+  int group = kMaxSeg;
   if (impl == HS_IMPL_LANE && d_ws != nullptr && ws_bytes >= kWorkspaceBytes && total > 0) {
     tk.ticket = reinterpret_cast<unsigned int*>(d_ws);
-    tk.acc = reinterpret_cast<unsigned long long*>(reinterpret_cast<uint8_t*>(d_ws) + 256);
+    tk.acc = reinterpret_cast<unsigned long long*>(reinterpret_cast<uint8_t*>(d_ws) + kTicketBytes);
+    group = int(std::min<size_t>(kMaxSeg, (ws_bytes - kTicketBytes) / (256 * sizeof(uint64_t))));
   } else {
     cudaError_t e = cudaMemsetAsync(d_out, 0, size_t(nseg) * 256 * sizeof(uint64_t), st);
     if (e != cudaSuccess) return fold(e);
   }
   if (total == 0) return HS_OK;
-  for (int s0 = 0; s0 < nseg; s0 += kMaxSeg) {
-    const int ns = std::min(kMaxSeg, nseg - s0);
+  for (int s0 = 0; s0 < nseg; s0 += group) {
+    const int ns = std::min(group, nseg - s0);
     bool empty = true;
     for (int i = 0; i < ns; ++i) empty = empty && h_end[s0 + i] == h_begin[s0 + i];
     if (empty && tk.ticket != nullptr) {
@@ -1403,7 +1412,7 @@ int hs_stream_step(const uint8_t* d_data, const uint64_t* h_begin, const uint64_
                    void* d_state, int window_size, double threshold, int recompute_every, int iteration,
                    uint64_t* d_out, double* d_deg_log, double* d_div_log, int32_t* d_kind_log,
                    uint64_t* d_ns_log, void* d_ws, size_t ws_bytes, void* stream) {
-  if (!d_state || window_size < 1 || nseg < 1 || nseg > kMaxSeg || recompute_every < 1 || iteration < 0 ||
+  if (!d_state || window_size < 1 || nseg < 1 || nseg > kMaxSegEngine || recompute_every < 1 || iteration < 0 ||
       !d_out || !d_deg_log || !d_div_log || !d_kind_log || !h_begin || !h_end)
     return HS_ERR_INVALID_ARG;
   if (!(threshold > 0.0 && threshold < 1.0)) return HS_ERR_INVALID_ARG;
@@ -1421,7 +1430,7 @@ int hs_stream_step(const uint8_t* d_data, const uint64_t* h_begin, const uint64_
   int rc = dev_info(di);
   if (rc != HS_OK) return rc;
   Tickets tk{reinterpret_cast<unsigned int*>(d_ws),
-             reinterpret_cast<unsigned long long*>(reinterpret_cast<uint8_t*>(d_ws) + 256)};
+             reinterpret_cast<unsigned long long*>(reinterpret_cast<uint8_t*>(d_ws) + kTicketBytes)};
   bool empty = total == 0;
   if (empty) {
     cudaError_t e = cudaMemsetAsync(d_out, 0, size_t(nseg) * 256 * sizeof(uint64_t), st);

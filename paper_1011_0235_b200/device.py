@@ -141,7 +141,7 @@ class Staging:
         share it must be stream-ordered (one staging per stream user)."""
         if self._ws is None:
             t = torch()
-            n = int(N.lib().hs_workspace_bytes(64))
+            n = int(N.lib().hs_workspace_bytes(256))  # launches of up to 256 segments
             self._ws = t.zeros(max(n, 256), dtype=t.uint8, device=self.device)
         return self._ws
 
