@@ -99,7 +99,7 @@ size_t hs_workspace_bytes(int nseg);
  *            for NAIVE; validated before launch (kernels.py:363).
  *   d_out    uint64[nseg*256], overwritten.
  *   d_ws     optional workspace of hs_workspace_bytes() bytes, zeroed once by the caller:
- *            the call is then ONE kernel launch per <= 64 segments (CTAs RED into
+ *            the call is then ONE kernel launch per <= 256 segments and 1 GiB (CTAs RED into
  *            workspace rows; the last CTA per segment stores d_out and re-zeroes its row).
  *            Without it a memset of d_out precedes the launch. Calls sharing a workspace
  *            must be stream-ordered.

@@ -274,7 +274,7 @@ def _with_hints(kind: int, pattern) -> int:
 def launch(staged: StagedBatch, kind: int, pattern=None, stream=None, impl: int = N.HS_IMPL_AUTO, out=None,
            staging: Staging | None = None):
     """hs_histogram_batched on ``stream`` (waits for the staging copies first): one
-    kernel launch per <= 64 segments, output written in-kernel through ``staging``'s
+    kernel launch per <= 256 segments and 1 GiB, output written in-kernel through ``staging``'s
     workspace. Returns the device int64 tensor [nseg, 256] (reinterpret as uint64)."""
     t = require_cuda()
     stream = stream or t.cuda.current_stream()
