@@ -636,9 +636,18 @@ __global__ void __launch_bounds__(kSubThreads)
   const uint32_t e = pp.entry[b], off = e & 0xffff, cnt = e >> 16;
   unsigned long long tot = 0;
   if (stage == HS_STAGE_SUBHIST_NOREDUCE) {
-    // sink = sum of every slot (kernels.py:462-463)
+    // sink = sum of every slot (kernels.py:462-463): reduced in the CTA first, so the
+    // stage pays one global atomic per CTA, not one per thread on a single address
     for (int i = threadIdx.x; i < 8 * S; i += blockDim.x) tot += slots[i];
-    if (tot) atomicAdd(sink, tot);
+    for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    __shared__ unsigned long long warp_tot[kSubThreads / 32];
+    if (lane == 0) warp_tot[warp] = tot;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long t = 0;
+      for (int w = 0; w < kSubThreads / 32; ++w) t += warp_tot[w];
+      if (t) atomicAdd(sink, t);
+    }
     return;
   }
   for (int w = 0; w < 8; ++w)
