@@ -1,5 +1,5 @@
 """Copy/compute overlap of the host-streamed pipeline (BASELINE configs[3] shape):
-pinned 16 MiB chunks, batches of 4, run_pipeline on a copy and a compute stream.
+pinned 16 MiB chunks, batches of 16 (256 MiB), run_pipeline on a copy and a compute stream.
 Writes profiles/<tag>_stream_timeline.csv and prints the overlap summary."""
 import sys
 from pathlib import Path
@@ -13,8 +13,8 @@ import paper_1011_0235_b200 as hs  # noqa: E402
 from paper_1011_0235_b200 import device as D  # noqa: E402
 
 tag = sys.argv[1] if len(sys.argv) > 1 else "r1"
-CHUNK, BATCH, ITERS = 16 << 20, 4, 32
-n = CHUNK * BATCH * ITERS  # 2 GiB, mixed schedule: uniform / normal / constant thirds
+CHUNK, BATCH, ITERS = 16 << 20, 16, 16
+n = CHUNK * BATCH * ITERS  # 4 GiB, mixed schedule: uniform / normal / constant thirds
 pinned = D.pinned_bytes(n)
 dev = torch.empty(n, dtype=torch.uint8, device="cuda")
 third = n // 3 // CHUNK * CHUNK
