@@ -6,7 +6,7 @@
 //   _adaptive_worker  kernels.py:133-168  -> k_lane<HOT> (HS_IMPL_LANE) / k_subbin (HS_IMPL_SUBBIN)
 //   reduce_subbins    kernels.py:410-418  -> fused flush epilogues below
 //   merge_all         core.py:152-156     -> u64 RED into d_out (integer adds commute: exact)
-//   batch_histograms  stream.py:260-316   -> one launch over up to kMaxSeg segments
+//   batch_histograms  stream.py:260-316   -> one launch per <= kMaxSeg segments and <= 1 GiB
 //   _adaptive_worker_traced / _u16        -> k_group_slots (reference group/lane mapping)
 //   _stage_*_worker   kernels.py:212-264  -> k_ablation
 //   _fill_*           datagen.py:98-133   -> k_gen_*
@@ -20,9 +20,12 @@
 //     degenerate data) and occupancy is unconstrained (2 CTAs = 64 warps per SM).
 //   * Blackwell merges same-address lanes of one shared atomic, so the contention the
 //     paper's AHist relieves (all lanes on one bin) is cheap here; what costs is distinct
-//     addresses in one bank. ADAPTIVE therefore keeps the lane-private core and uses the
-//     CPU pattern to pick the hot bin, whose all-hot 16-byte vectors are counted in a
+//     addresses in one bank. ADAPTIVE therefore keeps the lane-banked core; for a prior
+//     dominated by one value it counts that hot bin's all-hot 16-byte vectors in a
 //     register (no shared-memory traffic at all on degenerate input).
+//   * Launches are chained with programmatic dependent launch (griddepcontrol): a launch
+//     streams while the previous one's tail drains and waits only before its first
+//     global write. Output is ticketed: one kernel per launch, no memset.
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdlib>
