@@ -42,6 +42,11 @@ constexpr int kMaxSeg = 256;         // segments per launch (SegParams ~5 KB: la
 constexpr int kMaxSegEngine = 64;    // per hs_stream_step batch (the fold stages it in shared memory)
 constexpr size_t kTicketBytes = 1024;  // workspace head: kMaxSeg u32 tickets
 constexpr uint64_t kBigCap = 1ull << 30;  // u32 per-warp counters: far from wrapping
+// CTA ranges are whole multiples of 4 KiB of the launch's concatenated range: with
+// ranges cut at word granularity (1 GiB over 296 CTAs = 3,627,504 bytes each) a warp's
+// 512-byte vector load straddles five 128-byte lines instead of four, and a 1 GiB
+// launch took 162 us instead of 157 us (tools/size_sweep.py)
+constexpr uint64_t kSplitWords = 1024;
 
 struct SegParams {
   uint64_t begin[kMaxSeg];       // device byte offset of segment s
@@ -52,8 +57,9 @@ struct SegParams {
   // segments that continue in the next launch of the same call (bit s): their CTAs
   // only RED into the accumulator row; the launch holding a segment's end finalizes it
   uint32_t open_mask[kMaxSeg / 32];
-  // balanced split of the concatenated words over the grid, precomputed on the host
-  // (no 64-bit division on the device): CTA b owns q words, plus one if b < r
+  // balanced split of the concatenated range over the grid in kSplitWords units,
+  // precomputed on the host (no 64-bit division on the device): CTA b owns q units,
+  // plus one if b < r; the last unit may be partial
   uint64_t q, r;
   uint32_t ctas_after_first[kMaxSeg];  // (last CTA - first CTA) touching segment s
 };
@@ -143,9 +149,10 @@ __device__ __forceinline__ void block_range(uint64_t total, uint64_t& vb, uint64
 
 // The same split with the host's q, r (SegParams launches)
 __device__ __forceinline__ void block_range(const SegParams& sp, uint64_t& vb, uint64_t& ve) {
-  const uint64_t b = blockIdx.x;
-  vb = 4 * (sp.q * b + min(b, sp.r));
-  ve = vb + 4 * (sp.q + (b < sp.r ? 1 : 0));
+  const uint64_t b = blockIdx.x, total = sp.vstart[sp.nseg];
+  const uint64_t u0 = sp.q * b + min(b, sp.r), u1 = u0 + sp.q + (b < sp.r ? 1 : 0);
+  vb = min(total, 4 * kSplitWords * u0);
+  ve = min(total, 4 * kSplitWords * u1);
 }
 
 // Walks the pieces (segment index, device byte range) of the block's range and calls
@@ -1045,21 +1052,35 @@ int set_smem_once(K kernel, size_t bytes, std::atomic<uint64_t>& done) {
 
 // CTA index owning word w of the balanced split of tw words over g CTAs
 uint32_t cta_of_word(uint64_t w, uint64_t tw, uint64_t g) {
-  const uint64_t q = tw / g, r = tw % g;
-  if (w < r * (q + 1)) return uint32_t(w / (q + 1));
-  return uint32_t(r + (w - r * (q + 1)) / q);
+  const uint64_t units = (tw + kSplitWords - 1) / kSplitWords, u = w / kSplitWords;
+  const uint64_t q = units / g, r = units % g;
+  if (u < r * (q + 1)) return uint32_t(u / (q + 1));
+  return uint32_t(r + (u - r * (q + 1)) / q);
 }
 
 // fills the grid split of sp (q, r and the per-segment CTA spans the tickets count)
 void split_grid(SegParams& sp, int grid) {
   const uint64_t tw = sp.vstart[sp.nseg] >> 2, g = uint64_t(grid);
-  sp.q = tw / g;
-  sp.r = tw % g;
+  const uint64_t units = (tw + kSplitWords - 1) / kSplitWords;
+  sp.q = units / g;
+  sp.r = units % g;
   for (int s = 0; s < sp.nseg; ++s) {
     sp.ctas_after_first[s] = 0;
     if (sp.vstart[s + 1] > sp.vstart[s])
       sp.ctas_after_first[s] = cta_of_word((sp.vstart[s + 1] >> 2) - 1, tw, g) - cta_of_word(sp.vstart[s] >> 2, tw, g);
   }
+}
+
+// CTAs for a k_lane launch over v bytes (capped later by the resident slots). Each CTA
+// pays a fixed start (zero 32 KB of counters) and end (flush, tickets), so mid-size
+// launches run faster on fewer, longer CTAs; from ~384 MiB on every resident slot is
+// used. Per-launch times (tools/size_sweep.py, graph-replayed, aligned CTA ranges):
+//   16 MiB: 64 CTAs 5.6 us (>= 64 KiB per CTA, 256 CTAs: 7.7 us)
+//   64 MiB: 128 CTAs 12.7 us (14.7 us);  1 GiB: 296 CTAs 154 us (256 CTAs: 159 us)
+uint64_t lane_grid_for(uint64_t v) {
+  if (v <= (48ull << 20)) return std::max<uint64_t>(1, std::min<uint64_t>(64, (v + (256ull << 10) - 1) >> 18));
+  if (v <= (384ull << 20)) return 128;
+  return ~0ull;  // every resident slot
 }
 
 // one launch over the <= kMaxSeg (pieces of) segments prepared in sp
@@ -1070,8 +1091,7 @@ int launch_batch(const uint8_t* d_data, SegParams& sp, int kind, int impl, const
   if (v == 0) return HS_OK;
   cudaError_t e = cudaSuccess;
   if (impl == HS_IMPL_LANE) {
-    // ~64 KiB of input per CTA at least; at most 2 resident CTAs per SM
-    const uint64_t want = (v + (64ull << 10) - 1) / (64ull << 10);
+    const uint64_t want = lane_grid_for(v);
     // reserve_slots CTA slots are left free (the device stream engine's fold CTA takes
     // one while the next histogram streams, instead of delaying one of its CTAs)
     const bool hot = kind == HS_KIND_ADAPTIVE && pp != nullptr && pp->hot_unique;
