@@ -41,6 +41,7 @@ sys.path.insert(0, str(ROOT))
 
 GiB = 1 << 30
 CHUNK = 16 << 20
+READ_ONLY_CEILING_GBS = 6973.3  # profiles/r1_mapping.txt (grid-stride read, 64 GiB)
 SIGMAS = (8.0, 32.0, 64.0)
 MEAN = 128.0
 BASE_SEED = 0x1011_0235
@@ -471,6 +472,10 @@ def main(argv=None):
             traffic = None
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
+                # context: the copy-derived peak counts read + write traffic; a read-only
+                # streaming kernel (tools/microbench/spread.cu, grid-stride, 64 GiB) reaches
+                # this on the same boxes, the ceiling for a 1-byte-read-per-pixel kernel
+                "read_only_ceiling_gbs": READ_ONLY_CEILING_GBS,
                 "achieved_method": "1 GiB / mean launch duration (CUDA events around 10 back-to-back launches per sigma stream, after warm-up, before the timed region)",
                 "concurrent_streams_gbs": round(value / world, 1),
                 "kernel": "k_lane, kind ADAPTIVE (hs_histogram_batched, 64 x 16 MiB segments)",

@@ -141,10 +141,12 @@ __device__ __forceinline__ uint32_t byte_of(uint32_t w, int k) { return __byte_p
 // ------------------------------------------------------------------ segment walk
 // Block b owns the word-aligned virtual range [vb, ve) of the concatenated segments.
 __device__ __forceinline__ void block_range(uint64_t total, uint64_t& vb, uint64_t& ve) {
-  const uint64_t tw = total >> 2, g = gridDim.x, b = blockIdx.x;
-  const uint64_t q = tw / g, r = tw % g;
-  vb = 4 * (q * b + min(b, r));
-  ve = vb + 4 * (q + (b < r ? 1 : 0));
+  // whole kSplitWords units per CTA, as the SegParams split below (line-aligned loads)
+  const uint64_t units = ((total >> 2) + kSplitWords - 1) / kSplitWords, g = gridDim.x, b = blockIdx.x;
+  const uint64_t q = units / g, r = units % g;
+  const uint64_t u0 = q * b + min(b, r), u1 = u0 + q + (b < r ? 1 : 0);
+  vb = min(total & ~uint64_t(3), 4 * kSplitWords * u0);
+  ve = min(total & ~uint64_t(3), 4 * kSplitWords * u1);
 }
 
 // The same split with the host's q, r (SegParams launches)
