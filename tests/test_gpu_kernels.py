@@ -388,3 +388,39 @@ def test_graph_replay_ticketed(cuda, oracle):
             for k in range(3):
                 assert got[k].tolist() == parts[k].tolist()
     assert not ws.any().item()
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_fuzz_segment_layouts(cuda, seed):
+    """Random batches through the C ABI: 1-300 segments of random word-multiple sizes
+    (empty ones included) at random word offsets of one buffer, every impl and kind,
+    with a workspace sized for 64 or 256 segments or none. Counts equal numpy's."""
+    torch = cuda
+    rng = np.random.default_rng(1000 + seed)
+    n = 48 << 20
+    host = rng.integers(0, 256, n, dtype=np.uint8)
+    host[: n // 3] = rng.integers(120, 136, n // 3, dtype=np.uint8)  # a concentrated stretch
+    buf = torch.from_numpy(host).cuda()
+    L = N.lib()
+    st = torch.cuda.current_stream().cuda_stream
+    pat = hs.compute_binning_pattern(hs.Histogram256(np.bincount(host[:1 << 20], minlength=256).astype(np.uint64)))
+    for trial in range(12):
+        nseg = int(rng.choice([1, 2, 7, 64, 65, 200, 256, 300]))
+        sizes = rng.choice([0, 4, 64, 4096, 1 << 16, 1 << 20, 3 << 20], size=nseg) + 4 * rng.integers(0, 64, nseg)
+        sizes[rng.random(nseg) < 0.1] = 0
+        starts = 4 * rng.integers(0, (n - int(sizes.max()) - 4) // 4, nseg)
+        b0 = starts.astype(np.uint64)
+        b1 = (starts + sizes).astype(np.uint64)
+        want = np.stack([np.bincount(host[a:b], minlength=256) for a, b in zip(b0, b1)]).astype(np.uint64)
+        impl = int(rng.choice([N.HS_IMPL_AUTO, N.HS_IMPL_LANE, N.HS_IMPL_WARP]))
+        kind = int(rng.choice([N.HS_KIND_NAIVE, N.HS_KIND_ADAPTIVE]))
+        ws_seg = int(rng.choice([0, 64, 256]))
+        ws = torch.zeros(int(L.hs_workspace_bytes(ws_seg)) if ws_seg else 1, dtype=torch.uint8, device="cuda")
+        out = torch.full((nseg, 256), -1, dtype=torch.int64, device="cuda")
+        N.check(L.hs_histogram_batched(buf.data_ptr(), N.u64p(b0), N.u64p(b1), nseg, kind, impl,
+                                       N.i64p(pat.offset), N.i64p(pat.count), 960, 8, out.data_ptr(),
+                                       ws.data_ptr() if ws_seg else None, ws.numel() if ws_seg else 0, st), "fuzz")
+        got = out.cpu().numpy().view(np.uint64)
+        assert np.array_equal(got, want), (seed, trial, nseg, impl, kind, ws_seg)
+        if ws_seg:
+            assert not ws.any().item()
