@@ -424,3 +424,32 @@ def test_fuzz_segment_layouts(cuda, seed):
         assert np.array_equal(got, want), (seed, trial, nseg, impl, kind, ws_seg)
         if ws_seg:
             assert not ws.any().item()
+
+
+def test_concurrent_streams_separate_workspaces(cuda, oracle):
+    """The bench's arrangement: three CUDA streams, each with its own workspace, each
+    issuing chained (PDL) 64-segment launches while the others run; every output exact."""
+    torch = cuda
+    L = N.lib()
+    seg = 1 << 20
+    bufs, wants = [], []
+    for j in range(3):
+        host = oracle.generate("normal", 64 * seg, 40 + j, mean=128.0, sigma=8.0 * (j + 1))
+        bufs.append(torch.from_numpy(host).cuda())
+        wants.append(np.stack([oracle.histogram(host[c * seg:(c + 1) * seg]) for c in range(64)]))
+    b0 = np.arange(64, dtype=np.uint64) * seg
+    b1 = b0 + seg
+    streams = [torch.cuda.Stream() for _ in range(3)]
+    wss = [torch.zeros(int(L.hs_workspace_bytes(64)), dtype=torch.uint8, device="cuda") for _ in range(3)]
+    outs = [[torch.full((64, 256), -1, dtype=torch.int64, device="cuda") for _ in range(5)] for _ in range(3)]
+    torch.cuda.synchronize()
+    for k in range(5):
+        for j in range(3):
+            N.check(L.hs_histogram_batched(bufs[j].data_ptr(), N.u64p(b0), N.u64p(b1), 64, N.HS_KIND_NAIVE,
+                                           N.HS_IMPL_LANE, None, None, 0, 0, outs[j][k].data_ptr(),
+                                           wss[j].data_ptr(), wss[j].numel(), streams[j].cuda_stream), "concurrent")
+    torch.cuda.synchronize()
+    for j in range(3):
+        for k in range(5):
+            assert np.array_equal(outs[j][k].cpu().numpy().view(np.uint64), wants[j]), (j, k)
+        assert not wss[j].any().item()
