@@ -261,9 +261,10 @@ __device__ __forceinline__ EachVec<U, VecFn> each_vec(VecFn& f) { return EachVec
 // Per byte: PRMT (extract) + IMAD (address) + ATOMS.POPC.INC.
 // A column (lane) adds at most piece/32 per flush; pieces are capped at 1 GiB per CTA.
 // Plain form: threads per CTA and resident CTAs per SM. Measured alternatives at the
-// same 64 warps/SM (tools/size_sweep.py, 1 GiB launches): 672 x 3 -> 171 us, 512 x 4 ->
-// 184 us, against 162 us here; each CTA brings its own 32 KB counter array, and more
-// arrays per SM slow the shared atomics (as did two arrays per CTA).
+// same 64 warps/SM (tools/size_sweep.py, 1 GiB launches, before the 4 KiB-aligned
+// split): 672 x 3 -> 171 us, 512 x 4 -> 184 us, against 162 us here; each CTA brings
+// its own 32 KB counter array, and more arrays per SM slow the shared atomics (as did
+// two arrays per CTA).
 #ifndef HS_LANE_THREADS
 #define HS_LANE_THREADS 1024
 #define HS_LANE_BLOCKS 2
@@ -286,11 +287,10 @@ struct Tickets {
 
 
 // Adds the CTA's counters into dst[256] (the output row, or the segment's accumulator
-// row of a ticketed launch) and re-zeroes them: 4 threads per bin, each summing 8 of
-// the bin's 32 lane words (staggered: conflict free), shuffle-combined. No fence here:
-// a mid-range flush must not wait for its REDs to reach L2 (that round trip under a
-// saturated memory system was ~6 us per CTA; tools/ab_seg.py), so the fence and the
-// tickets are taken once per CTA at the end (lane_tickets).
+// row of a ticketed launch) and re-zeroes them unless this was the CTA's last piece:
+// 4 threads per bin, each summing 8 of the bin's 32 lane words (staggered: conflict
+// free), shuffle-combined. No fence here: the fence and the tickets are taken once per
+// CTA at the end (lane_tickets), after all of its flushes.
 __device__ __forceinline__ void lane_flush(uint32_t sbase, unsigned long long* __restrict__ dst, bool rezero) {
   compiler_fence();
   __syncthreads();
