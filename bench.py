@@ -366,7 +366,8 @@ def main(argv=None):
         reps = 10
         per_sigma = {}
         ev = []
-        torch.cuda._sleep(50_000_000)
+        with torch.cuda.stream(s0):
+            torch.cuda._sleep(50_000_000)  # holds s0 while all 30 launches are enqueued
         for j in range(len(SIGMAS)):
             p = patterns[j]
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

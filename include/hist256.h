@@ -111,8 +111,13 @@ int hs_histogram_batched(const uint8_t* d_data, const uint64_t* h_begin, const u
                          int64_t total_slots, int64_t cap,
                          uint64_t* d_out, void* d_ws, size_t ws_bytes, void* stream);
 
-/* hs_histogram_batched, then the D2H of d_out[nseg][256] into h_out and a wait for the
- * stream: the synchronous API path for device-resident chunks in one call. Blocking. */
+/* hs_histogram_batched, then the counts into h_out[nseg][256] and a wait for the stream:
+ * the synchronous API path for device-resident chunks in one call. Blocking.
+ * The launch grid is sized for latency (>= 16 KiB per CTA) rather than for
+ * back-to-back throughput. When h_out is page-locked (cudaHostAlloc, torch
+ * pin_memory, cudaHostRegister) and the call is ticketed (HS_IMPL_AUTO/LANE with
+ * d_ws), each segment's last CTA writes its counts straight into h_out and d_out is
+ * not written; otherwise the counts go to d_out and are copied to h_out. */
 int hs_histogram_sync(const uint8_t* d_data, const uint64_t* h_begin, const uint64_t* h_end, int nseg,
                       int kind, int impl, const int64_t* h_offset, const int64_t* h_count,
                       int64_t total_slots, int64_t cap, uint64_t* d_out, uint64_t* h_out,
@@ -125,7 +130,8 @@ int hs_histogram_sync(const uint8_t* d_data, const uint64_t* h_begin, const uint
  * d_ws, copies d_out[nseg][256] into h_out and waits for the stream. Everything else as
  * hs_histogram_batched. d_stage must hold the chunks rounded up to 16 bytes each
  * (HS_ERR_WORKSPACE otherwise). One call instead of a copy, a launch and a readback
- * issued from Python: a 1 MiB image costs about half. Blocking. */
+ * issued from Python: a 1 MiB image costs about half. Blocking. Grid and h_out as
+ * hs_histogram_sync (a page-locked h_out is written by the kernel directly). */
 int hs_histogram_host(const uint8_t* const* h_chunks, const uint64_t* h_sizes, int nseg, int kind, int impl,
                       const int64_t* h_offset, const int64_t* h_count, int64_t total_slots, int64_t cap,
                       uint8_t* d_stage, size_t stage_bytes, uint64_t* d_out, uint64_t* h_out,

@@ -1079,8 +1079,13 @@ void split_grid(SegParams& sp, int grid) {
 // used. Per-launch times (tools/size_sweep.py, graph-replayed, aligned CTA ranges):
 //   16 MiB: 64 CTAs 5.6 us (>= 64 KiB per CTA, 256 CTAs: 7.7 us)
 //   64 MiB: 128 CTAs 12.7 us (14.7 us);  1 GiB: 296 CTAs 154 us (256 CTAs: 159 us)
-uint64_t lane_grid_for(uint64_t v) {
-  if (v <= (48ull << 20)) return std::max<uint64_t>(1, std::min<uint64_t>(64, (v + (256ull << 10) - 1) >> 18));
+// The blocking entries (hs_histogram_sync / hs_histogram_host) wait for the one launch,
+// so there the grid is sized for latency instead: >= 16 KiB per CTA below 48 MiB. On a
+// 1024x1024 image that is 64 CTAs instead of 4: 28 -> 18 us per blocking call, while
+// graph-replayed back-to-back launches lose 3% (tools/c1_breakdown.py).
+uint64_t lane_grid_for(uint64_t v, bool latency = false) {
+  const int shift = latency ? 14 : 18;
+  if (v <= (48ull << 20)) return std::max<uint64_t>(1, std::min<uint64_t>(64, (v + (1ull << shift) - 1) >> shift));
   if (v <= (384ull << 20)) return 128;
   return ~0ull;  // every resident slot
 }
@@ -1088,12 +1093,12 @@ uint64_t lane_grid_for(uint64_t v) {
 // one launch over the <= kMaxSeg (pieces of) segments prepared in sp
 int launch_batch(const uint8_t* d_data, SegParams& sp, int kind, int impl, const PatternParams* pp,
                  unsigned long long* d_out, cudaStream_t st, const DevInfo& di, const Tickets& tk,
-                 int reserve_slots = 0) {
+                 int reserve_slots = 0, bool latency = false) {
   const uint64_t v = sp.vstart[sp.nseg];
   if (v == 0) return HS_OK;
   cudaError_t e = cudaSuccess;
   if (impl == HS_IMPL_LANE) {
-    const uint64_t want = lane_grid_for(v);
+    const uint64_t want = lane_grid_for(v, latency);
     // reserve_slots CTA slots are left free (the device stream engine's fold CTA takes
     // one while the next histogram streams, instead of delaying one of its CTAs)
     const bool hot = kind == HS_KIND_ADAPTIVE && pp != nullptr && pp->hot_unique;
@@ -1160,7 +1165,7 @@ constexpr uint64_t kLaunchBytes = 1ull << 30;  // a word multiple, so every cut 
 
 int launch_segments(const uint8_t* d_data, const uint64_t* h_begin, const uint64_t* h_end, int s0, int ns,
                     int kind, int impl, const PatternParams* pp, unsigned long long* d_out, cudaStream_t st,
-                    const DevInfo& di, const Tickets& tk, int reserve_slots = 0) {
+                    const DevInfo& di, const Tickets& tk, int reserve_slots = 0, bool latency = false) {
   uint64_t vs[kMaxSeg + 1];
   vs[0] = 0;
   for (int i = 0; i < ns; ++i) vs[i + 1] = vs[i] + (h_end[s0 + i] - h_begin[s0 + i]);
@@ -1188,7 +1193,7 @@ int launch_segments(const uint8_t* d_data, const uint64_t* h_begin, const uint64
       if (vs[i + 1] > v1) sp.open_mask[k >> 5] |= 1u << (k & 31);
     }
     sp.out_base = s0 + sp.acc_base;
-    int rc = launch_batch(d_data, sp, kind, impl, pp, d_out, st, di, tk, reserve_slots);
+    int rc = launch_batch(d_data, sp, kind, impl, pp, d_out, st, di, tk, reserve_slots, latency);
     if (rc != HS_OK) return rc;
   }
   return HS_OK;
@@ -1246,10 +1251,12 @@ size_t hs_workspace_bytes(int nseg) {
   return nseg < 0 ? 0 : ws_bytes_for(std::max(kMaxSegEngine, std::min(nseg, kMaxSeg)));
 }
 
-int hs_histogram_batched(const uint8_t* d_data, const uint64_t* h_begin, const uint64_t* h_end, int nseg,
-                         int kind, int impl, const int64_t* h_offset, const int64_t* h_count,
-                         int64_t total_slots, int64_t cap, uint64_t* d_out, void* d_ws, size_t ws_bytes,
-                         void* stream) {
+}  // extern "C"
+
+namespace {
+int histogram_batched(const uint8_t* d_data, const uint64_t* h_begin, const uint64_t* h_end, int nseg, int kind,
+                      int impl, const int64_t* h_offset, const int64_t* h_count, int64_t total_slots, int64_t cap,
+                      uint64_t* d_out, void* d_ws, size_t ws_bytes, void* stream, bool latency) {
   if (nseg < 0 || (nseg > 0 && (!h_begin || !h_end || !d_out))) return HS_ERR_INVALID_ARG;
   const bool spread = (kind & HS_KIND_FLAG_SPREAD) != 0;
   kind &= ~HS_KIND_FLAG_SPREAD;
@@ -1300,21 +1307,64 @@ int hs_histogram_batched(const uint8_t* d_data, const uint64_t* h_begin, const u
       continue;
     }
     rc = launch_segments(d_data, h_begin, h_end, s0, ns, kind, impl, have_pattern ? &pp : nullptr,
-                         reinterpret_cast<unsigned long long*>(d_out), st, di, tk);
+                         reinterpret_cast<unsigned long long*>(d_out), st, di, tk, 0, latency);
     if (rc != HS_OK) return rc;
   }
   return HS_OK;
 }
+}  // namespace
+
+extern "C" {
+
+int hs_histogram_batched(const uint8_t* d_data, const uint64_t* h_begin, const uint64_t* h_end, int nseg,
+                         int kind, int impl, const int64_t* h_offset, const int64_t* h_count,
+                         int64_t total_slots, int64_t cap, uint64_t* d_out, void* d_ws, size_t ws_bytes,
+                         void* stream) {
+  return histogram_batched(d_data, h_begin, h_end, nseg, kind, impl, h_offset, h_count, total_slots, cap, d_out,
+                           d_ws, ws_bytes, stream, false);
+}
+
+}  // extern "C"
+
+namespace {
+// Device view of a page-locked h_out, or nullptr. The blocking entries let the kernel
+// write the counts straight into page-locked host memory (one PCIe write of 2 KiB per
+// segment from the segment's last CTA) instead of a D2H copy after it: only on the
+// ticketed path, whose output is plain stores (the memset + RED path would put
+// atomics on host memory).
+uint64_t* mapped_host_out(uint64_t* h_out, int impl, void* d_ws, size_t ws_bytes) {
+#ifndef HS_NO_DIRECT_HOST_OUT
+  if ((impl != HS_IMPL_AUTO && impl != HS_IMPL_LANE) || !d_ws || ws_bytes < kWorkspaceBytes) return nullptr;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, h_out) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  if (a.type != cudaMemoryTypeHost || a.devicePointer == nullptr) return nullptr;
+  return reinterpret_cast<uint64_t*>(a.devicePointer);
+#else
+  (void)h_out; (void)impl; (void)d_ws; (void)ws_bytes;
+  return nullptr;
+#endif
+}
+}  // namespace
+
+extern "C" {
 
 int hs_histogram_sync(const uint8_t* d_data, const uint64_t* h_begin, const uint64_t* h_end, int nseg,
                       int kind, int impl, const int64_t* h_offset, const int64_t* h_count,
                       int64_t total_slots, int64_t cap, uint64_t* d_out, uint64_t* h_out,
                       void* d_ws, size_t ws_bytes, void* stream) {
   if (nseg > 0 && !h_out) return HS_ERR_INVALID_ARG;
-  int rc = hs_histogram_batched(d_data, h_begin, h_end, nseg, kind, impl, h_offset, h_count, total_slots, cap,
-                                d_out, d_ws, ws_bytes, stream);
-  if (rc != HS_OK || nseg == 0) return rc;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (uint64_t* m = nseg > 0 ? mapped_host_out(h_out, impl, d_ws, ws_bytes) : nullptr) {
+    int rc = histogram_batched(d_data, h_begin, h_end, nseg, kind, impl, h_offset, h_count, total_slots, cap, m,
+                               d_ws, ws_bytes, stream, true);
+    return rc != HS_OK ? rc : fold(cudaStreamSynchronize(st));
+  }
+  int rc = histogram_batched(d_data, h_begin, h_end, nseg, kind, impl, h_offset, h_count, total_slots, cap, d_out,
+                             d_ws, ws_bytes, stream, true);
+  if (rc != HS_OK || nseg == 0) return rc;
   cudaError_t e = cudaMemcpyAsync(h_out, d_out, size_t(nseg) * 256 * sizeof(uint64_t), cudaMemcpyDeviceToHost, st);
   if (e != cudaSuccess) return fold(e);
   return fold(cudaStreamSynchronize(st));
@@ -1342,8 +1392,13 @@ int hs_histogram_host(const uint8_t* const* h_chunks, const uint64_t* h_sizes, i
     cudaError_t e = cudaMemcpyAsync(d_stage + begin[s], h_chunks[s], h_sizes[s], cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) return fold(e);
   }
-  int rc = hs_histogram_batched(d_stage, begin.data(), end.data(), nseg, kind, impl, h_offset, h_count, total_slots,
-                                cap, d_out, d_ws, ws_bytes, stream);
+  if (uint64_t* m = mapped_host_out(h_out, impl, d_ws, ws_bytes)) {
+    int rc = histogram_batched(d_stage, begin.data(), end.data(), nseg, kind, impl, h_offset, h_count,
+                               total_slots, cap, m, d_ws, ws_bytes, stream, true);
+    return rc != HS_OK ? rc : fold(cudaStreamSynchronize(st));
+  }
+  int rc = histogram_batched(d_stage, begin.data(), end.data(), nseg, kind, impl, h_offset, h_count, total_slots,
+                             cap, d_out, d_ws, ws_bytes, stream, true);
   if (rc != HS_OK) return rc;
   cudaError_t e = cudaMemcpyAsync(h_out, d_out, size_t(nseg) * 256 * sizeof(uint64_t), cudaMemcpyDeviceToHost, st);
   if (e != cudaSuccess) return fold(e);

@@ -126,6 +126,7 @@ class Staging:
         self._out_host = None
         self._out_dev = None
         self._ws = None
+        self._one = None  # _OneCall: prepared arguments of the one-chunk blocking calls
 
     def device_bytes(self, n: int):
         t = torch()
@@ -158,6 +159,46 @@ class Staging:
         if self._out_host is None or self._out_host.numel() < need:
             self._out_host = t.empty(max(need, 64 * BINS), dtype=t.int64, pin_memory=True)
         return self._out_host[:need]
+
+    def one_call(self, n_bytes: int = 0) -> "_OneCall":
+        """Arguments of one-chunk blocking calls (the per-image path), built once: the
+        device, host and workspace buffers are only ever replaced by larger ones, so
+        the cached pointers stay valid until a buffer grows."""
+        one = self._one
+        if (one is None or one.out_dev is not self._out_dev or one.h_out is not self._out_host
+                or one.dev is not self._dev or (n_bytes and (self._dev is None or self._dev.numel() < n_bytes))):
+            if n_bytes:
+                self.device_bytes(n_bytes)
+            one = self._one = _OneCall(self, self.device_out(1), self.host_out(1), self.workspace(), self._dev)
+        return one
+
+
+class _OneCall:
+    """ctypes arguments of hs_histogram_sync / hs_histogram_host for one chunk."""
+
+    def __init__(self, staging: Staging, out_dev, h_out, ws, dev):
+        self.out_dev = staging._out_dev  # the owning tensors (identity = validity)
+        self.h_out = staging._out_host
+        self.dev = staging._dev
+        self.out_dev_ptr = out_dev.data_ptr()
+        self.h_np = h_out.numpy().view(np.uint64)
+        self.h_out_p = ctypes.cast(h_out.data_ptr(), N._U64P)
+        self.ws_ptr, self.ws_n = ws.data_ptr(), ws.numel()
+        self.dev_ptr, self.dev_n = (dev.data_ptr(), dev.numel()) if dev is not None else (None, 0)
+        self.begin = (ctypes.c_uint64 * 1)(0)
+        self.end = (ctypes.c_uint64 * 1)(0)
+        self.ptrs = (ctypes.c_void_p * 1)()
+        self.pattern = None
+        self.pattern_args = (None, None, 0, 0)
+
+    def pattern_ptrs(self, pattern):
+        if pattern is None:
+            return None, None, 0, 0
+        if pattern is not self.pattern:  # patterns are immutable; keep it alive with its pointers
+            self.pattern = pattern
+            self.pattern_args = (N.i64p(pattern.offset), N.i64p(pattern.count), int(pattern.total_slots),
+                                 int(pattern.cap))
+        return self.pattern_args
 
 
 @dataclass
@@ -332,8 +373,10 @@ def default_staging() -> Staging:
 def histograms(chunks: Sequence, kind: int, pattern=None, impl: int = N.HS_IMPL_AUTO) -> np.ndarray:
     """Synchronous batched histograms of host/device chunks -> uint64 [n, 256]."""
     t = require_cuda()
-    stream = t.cuda.current_stream()
     st = default_staging()
+    if len(chunks) == 1 and type(chunks[0]) in (PackedChunk, DeviceChunk):
+        return _one_histogram(chunks[0], kind, pattern, impl, st)[None, :]
+    stream = t.cuda.current_stream()
     if chunks and all(type(c) is PackedChunk for c in chunks):
         return _host_histograms(chunks, kind, pattern, impl, st, stream)
     if chunks and all(type(c) is DeviceChunk for c in chunks):
@@ -342,6 +385,36 @@ def histograms(chunks: Sequence, kind: int, pattern=None, impl: int = N.HS_IMPL_
     staged = stage(chunks, st, stream)
     out = launch(staged, kind, pattern, stream, impl, staging=st)
     return readback(out, st, stream)
+
+
+def _one_histogram(chunk, kind, pattern, impl, st: "Staging") -> np.ndarray:
+    """One chunk (the per-image path of naive_histogram / adaptive_histogram) through
+    the blocking native entries with arguments prepared once per staging: on a
+    1024x1024 image, marshalling the arguments anew each call cost as much as the
+    launch, kernel, readback and wait together (tools/c1_breakdown.py)."""
+    t = torch()
+    stream = t._C._cuda_getCurrentRawStream(st.device.index)
+    kind = int(_with_hints(kind, pattern))
+    if type(chunk) is DeviceChunk:
+        one = st.one_call()
+        off_p, cnt_p, S, cap = one.pattern_ptrs(pattern)
+        n = chunk._n
+        one.end[0] = n
+        status = N.lib().hs_histogram_sync(chunk._ptr if n else None, one.begin, one.end, 1, kind, int(impl),
+                                           off_p, cnt_p, S, cap, one.out_dev_ptr, one.h_out_p, one.ws_ptr,
+                                           one.ws_n, stream)
+        N.check(status, "hs_histogram_sync")
+    else:
+        n = chunk.byte_size
+        one = st.one_call(max(n, 16))
+        off_p, cnt_p, S, cap = one.pattern_ptrs(pattern)
+        one.end[0] = n
+        one.ptrs[0] = chunk.words.ctypes.data if n else None
+        status = N.lib().hs_histogram_host(one.ptrs, one.end, 1, kind, int(impl), off_p, cnt_p, S, cap,
+                                           one.dev_ptr, one.dev_n, one.out_dev_ptr, one.h_out_p, one.ws_ptr,
+                                           one.ws_n, stream)
+        N.check(status, "hs_histogram_host")
+    return one.h_np[:BINS].copy()
 
 
 def _host_histograms(chunks, kind, pattern, impl, st: "Staging", stream) -> np.ndarray:

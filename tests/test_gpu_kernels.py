@@ -453,3 +453,97 @@ def test_concurrent_streams_separate_workspaces(cuda, oracle):
         for k in range(5):
             assert np.array_equal(outs[j][k].cpu().numpy().view(np.uint64), wants[j]), (j, k)
         assert not wss[j].any().item()
+
+
+def _sync_call(lib, d, begin, end, h_out, d_out, ws, impl=N.HS_IMPL_AUTO):
+    import torch
+
+    b = np.ascontiguousarray(begin, np.uint64)
+    e = np.ascontiguousarray(end, np.uint64)
+    import ctypes
+
+    h_p = N.u64p(h_out) if isinstance(h_out, np.ndarray) else ctypes.cast(h_out.data_ptr(), N._U64P)
+    st = lib.hs_histogram_sync(d.data_ptr(), N.u64p(b), N.u64p(e), len(b), N.HS_KIND_NAIVE, impl, None, None, 0, 0,
+                               d_out.data_ptr(), h_p, ws.data_ptr() if ws is not None else None,
+                               ws.numel() if ws is not None else 0, torch.cuda.current_stream().cuda_stream)
+    N.check(st, "hs_histogram_sync")
+
+
+def test_blocking_entries_host_out_forms(cuda, oracle):
+    """hs_histogram_sync / hs_histogram_host with a page-locked h_out (written by the
+    kernel directly on the ticketed path), a pageable h_out (D2H copy), a non-ticketed
+    impl and no workspace with a page-locked h_out (copy path), including empty and
+    all-empty segment lists; the counts must be the same in every form."""
+    import ctypes
+    import torch
+
+    lib = N.lib()
+    rng = np.random.default_rng(11)
+    px = rng.integers(0, 256, (3 << 20) + 40, dtype=np.uint8)
+    d = torch.from_numpy(px).cuda()
+    cuts = [0, 4, 4, 1 << 20, (1 << 20) + 4, (3 << 20) + 40]
+    begin, end = cuts[:-1], cuts[1:]
+    want = np.stack([oracle.histogram(px[a:b]) for a, b in zip(begin, end)])
+    ws = torch.zeros(int(lib.hs_workspace_bytes(64)), dtype=torch.uint8, device="cuda")
+    n = len(begin)
+    for h_kind in ("pinned", "pageable"):
+        for impl, use_ws in ((N.HS_IMPL_AUTO, True), (N.HS_IMPL_LANE, True), (N.HS_IMPL_WARP, True),
+                             (N.HS_IMPL_AUTO, False)):
+            d_out = torch.full((n, 256), 7, dtype=torch.int64, device="cuda")
+            if h_kind == "pinned":
+                h = torch.full((n * 256,), 9, dtype=torch.int64).pin_memory()
+                _sync_call(lib, d, begin, end, h, d_out, ws if use_ws else None, impl)
+                got = h.numpy().view(np.uint64).reshape(n, 256)
+            else:
+                got = np.full((n, 256), 9, np.uint64)
+                _sync_call(lib, d, begin, end, got, d_out, ws if use_ws else None, impl)
+            assert np.array_equal(got, want), (h_kind, impl, use_ws)
+    # all-empty list and an empty device chunk through the pinned direct form
+    h = torch.full((2 * 256,), 9, dtype=torch.int64).pin_memory()
+    _sync_call(lib, d, [0, 8], [0, 8], h, torch.empty((2, 256), dtype=torch.int64, device="cuda"), ws)
+    assert not h.numpy().any()
+    # hs_histogram_host: pinned and pageable h_out, pageable sources
+    chunks = [px[:1 << 20], px[(1 << 20) + 4:(2 << 20)], px[:0]]
+    ptrs = (ctypes.c_void_p * 3)(*[c.ctypes.data if c.size else None for c in chunks])
+    sizes = np.array([c.size for c in chunks], np.uint64)
+    stage = torch.empty(4 << 20, dtype=torch.uint8, device="cuda")
+    d_out = torch.empty((3, 256), dtype=torch.int64, device="cuda")
+    want_h = np.stack([oracle.histogram(c) for c in chunks])
+    for pinned in (True, False):
+        h = torch.full((3 * 256,), 9, dtype=torch.int64)
+        if pinned:
+            h = h.pin_memory()
+        st = lib.hs_histogram_host(ptrs, N.u64p(sizes), 3, N.HS_KIND_NAIVE, N.HS_IMPL_AUTO, None, None, 0, 0,
+                                   stage.data_ptr(), stage.numel(), d_out.data_ptr(),
+                                   ctypes.cast(h.data_ptr(), N._U64P), ws.data_ptr(), ws.numel(),
+                                   torch.cuda.current_stream().cuda_stream)
+        N.check(st, "hs_histogram_host")
+        assert np.array_equal(h.numpy().view(np.uint64).reshape(3, 256), want_h), pinned
+
+
+def test_single_chunk_fast_path_buffers_regrow(cuda, oracle):
+    """The one-chunk API path caches its ctypes arguments per staging; a larger batch in
+    between replaces the staging buffers, and the next single call must use the new
+    ones (and a new pattern object its own pointers)."""
+    import torch
+
+    cfg = hs.WorkerGroupConfig()
+    px = oracle.generate("normal", (1 << 20) + 4, 5, mean=100.0, sigma=9.0)
+    host = hs.PackedChunk(oracle.pack(px))
+    dev = hs.DeviceChunk(torch.from_numpy(px).cuda())
+    want = oracle.histogram(px)
+    p1 = hs.compute_binning_pattern(hs.Histogram256(want))
+    for _ in range(2):
+        assert np.array_equal(hs.naive_histogram(host, cfg).counts, want)
+        assert np.array_equal(hs.adaptive_histogram(dev, p1, cfg).counts, want)
+        big = [hs.PackedChunk(oracle.pack(oracle.generate("uniform", 1 << 16, s))) for s in range(300)]
+        outs = hs.batch_histograms(big, hs.KernelKind.NAIVE, None, cfg)
+        assert all(o.total() == 1 << 16 for o in outs)
+        long_px = oracle.generate("uniform", 24 << 20, 3)
+        assert np.array_equal(hs.naive_histogram(hs.PackedChunk(oracle.pack(long_px)), cfg).counts,
+                              oracle.histogram(long_px))
+        p2 = hs.uniform_pattern(960)
+        assert np.array_equal(hs.adaptive_histogram(host, p2, cfg).counts, want)
+        assert np.array_equal(hs.adaptive_histogram(dev, p1, cfg).counts, want)
+        assert hs.naive_histogram(hs.PackedChunk(np.zeros(0, np.uint32)), cfg).total() == 0
+        assert hs.naive_histogram(hs.DeviceChunk(torch.empty(0, dtype=torch.uint8, device="cuda")), cfg).total() == 0
