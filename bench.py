@@ -498,7 +498,7 @@ def main(argv=None):
         torch.cuda.empty_cache()
     if rank == 0 and not args.no_extras:
         extra["c5_64gib_sharded"] = c5
-        extra["c1_image_1024x1024"] = c1_image(hs, N, torch, L, dev)
+        extra["c1_image_1024x1024"] = c1_image(hs, N, D, torch, L, dev)
         extra["c3_switch_stream"] = c3_switch(hs, torch, dev)
 
     if rank == 0:
@@ -531,9 +531,10 @@ def main(argv=None):
 C1_IMAGES = 256
 
 
-def c1_image(hs, N, torch, L, dev):
+def c1_image(hs, N, D, torch, L, dev):
     """BASELINE configs[0]: one 1024x1024 uniform image (seed 0). L2-resident and
-    launch-bound, so reported beside the headline: latency through the public API,
+    launch-bound, so reported beside the headline: latency through the public API
+    (pageable, pinned and device-resident chunk),
     256 images per call (one launch of 256 segments), and single-image launches
     replayed from a CUDA graph."""
     from oracle import oracle as O
@@ -546,10 +547,21 @@ def c1_image(hs, N, torch, L, dev):
     for _ in range(5):
         h = hs.naive_histogram(chunk, cfg)
     assert np.array_equal(h.counts, want)
-    t0 = time.perf_counter()
-    for _ in range(50):
-        hs.naive_histogram(chunk, cfg)
-    api_us = (time.perf_counter() - t0) / 50 * 1e6
+    def per_call_us(c, reps=200):
+        for _ in range(5):
+            hs.naive_histogram(c, cfg)
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            hs.naive_histogram(c, cfg)
+        return (time.perf_counter() - t0) / reps * 1e6
+
+    api_us = per_call_us(chunk)  # pageable numpy words, as the reference's callers hold them
+    pin = D.pinned_words(chunk.words.size)
+    pin[:] = chunk.words
+    pinned_us = per_call_us(hs.PackedChunk(pin))
+    dev_chunk = hs.DeviceChunk(torch.from_numpy(chunk.pixels().copy()).to(dev))
+    device_us = per_call_us(dev_chunk)
+    assert np.array_equal(hs.naive_histogram(dev_chunk, cfg).counts, want)
     # C1_IMAGES images, one call
     imgs = torch.empty(C1_IMAGES * n, dtype=torch.uint8, device=dev)
     for i in range(C1_IMAGES):
@@ -605,6 +617,7 @@ def c1_image(hs, N, torch, L, dev):
         O.naive_histogram(chunk.words, 32, host_cores())
     cpu_us = (time.perf_counter() - t0) / 5 * 1e6
     return {"bytes": n, "public_api_us_per_image": round(api_us, 2),
+            "public_api_pinned_us": round(pinned_us, 2), "public_api_device_chunk_us": round(device_us, 2),
             "batched_images": C1_IMAGES, "batched_us_per_image": round(batch_us / C1_IMAGES, 3),
             "batched_gbs": round(C1_IMAGES * n / (batch_us * 1e3), 1),
             "graph_single_image_us": round(graph_us, 3), "cpu_reference_port_us": round(cpu_us, 1)}
