@@ -48,6 +48,8 @@ constexpr uint64_t kBigCap = 1ull << 30;  // u32 per-warp counters: far from wra
 // launch took 162 us instead of 157 us (tools/size_sweep.py)
 constexpr uint64_t kSplitWords = 1024;
 
+constexpr int kMaxSplitGrid = 320;  // weighted split table size (>= 2 CTAs x 148 SMs)
+
 struct SegParams {
   uint64_t begin[kMaxSeg];       // device byte offset of segment s
   uint64_t vstart[kMaxSeg + 1];  // virtual (concatenated) start of segment s
@@ -61,8 +63,43 @@ struct SegParams {
   // precomputed on the host (no 64-bit division on the device): CTA b owns q units,
   // plus one if b < r; the last unit may be partial
   uint64_t q, r;
-  uint32_t ctas_after_first[kMaxSeg];  // (last CTA - first CTA) touching segment s
+  // Cost-weighted split (split_cost > 0, k_lane launches over several segments): a CTA
+  // whose range crosses a segment boundary flushes its counters there (barrier, drain
+  // of the load pipeline, 256 global REDs), so such a CTA is given split_cost fewer
+  // units. Cost(u) = u + split_cost * (boundaries before unit u); CTA b starts at the
+  // first unit whose cost reaches floor(b * Cost(units) / grid) = cq*b + cr*b/grid.
+  uint32_t split_cost;
+  uint32_t lead_empty;           // boundaries s >= 1 at virtual offset 0 (not counted)
+  uint64_t units;                // kSplitWords units of the launch
+  uint64_t cq;
+  uint32_t cr;
+  uint32_t ctas_after_first[kMaxSeg];  // CTAs with work in segment s, minus one
+  uint32_t cta_unit[kMaxSplitGrid + 1];  // weighted split: first unit of CTA b (host-computed)
 };
+
+// Cost of the first u units under the weighted split (host and device)
+__host__ __device__ __forceinline__ uint64_t split_cost_at(const SegParams& sp, uint64_t u) {
+  const uint64_t x = u * (4 * kSplitWords);
+  int lo = 1, hi = sp.nseg;  // first s in [1, nseg) with vstart[s] >= x
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (sp.vstart[mid] < x) lo = mid + 1; else hi = mid;
+  }
+  const uint32_t before = uint32_t(lo - 1);
+  const uint32_t nb = before > sp.lead_empty ? before - sp.lead_empty : 0u;
+  return u + uint64_t(sp.split_cost) * nb;
+}
+
+// First unit of CTA b (b == grid: the end) under the weighted split
+__host__ __device__ __forceinline__ uint64_t split_unit_of(const SegParams& sp, uint32_t b, uint32_t grid) {
+  const uint64_t t = sp.cq * b + (sp.cr * b) / grid;  // cr < grid <= a few thousand: 32-bit
+  uint64_t lo = 0, hi = sp.units;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (split_cost_at(sp, mid) < t) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
 
 struct PatternParams {
   uint32_t entry[256];           // offset | count << 16   (sub-bin kernels)
@@ -152,7 +189,14 @@ __device__ __forceinline__ void block_range(uint64_t total, uint64_t& vb, uint64
 // The same split with the host's q, r (SegParams launches)
 __device__ __forceinline__ void block_range(const SegParams& sp, uint64_t& vb, uint64_t& ve) {
   const uint64_t b = blockIdx.x, total = sp.vstart[sp.nseg];
-  const uint64_t u0 = sp.q * b + min(b, sp.r), u1 = u0 + sp.q + (b < sp.r ? 1 : 0);
+  uint64_t u0, u1;
+  if (sp.split_cost) {
+    u0 = sp.cta_unit[b];
+    u1 = sp.cta_unit[b + 1];
+  } else {
+    u0 = sp.q * b + min(b, sp.r);
+    u1 = u0 + sp.q + (b < sp.r ? 1 : 0);
+  }
   vb = min(total, 4 * kSplitWords * u0);
   ve = min(total, 4 * kSplitWords * u1);
 }
@@ -1060,12 +1104,47 @@ uint32_t cta_of_word(uint64_t w, uint64_t tw, uint64_t g) {
   return uint32_t(r + (u - r * (q + 1)) / q);
 }
 
-// fills the grid split of sp (q, r and the per-segment CTA spans the tickets count)
-void split_grid(SegParams& sp, int grid) {
+// Units a segment boundary inside a CTA's range costs that CTA (the weighted split of
+// k_lane launches over several segments). 0 = plain split. Per 1 GiB launch
+// (tools/split_cost_ab.py, profiles/r1_split_cost_ab.txt), plain -> 32: 16 x 64 MiB
+// 158.7 -> 157.0 us, 64 x 16 MiB 158.7 -> 158.3, 64 random sizes 161.2 -> 158.8; one
+// segment 156.7. The split is a host-computed table in the launch parameters: computing
+// it on the device (binary searches by thread 0 before the first load) cost 2 us.
+#ifndef HS_SPLIT_COST
+#define HS_SPLIT_COST 32
+#endif
+constexpr uint32_t kLaneSplitCost = HS_SPLIT_COST;
+
+// fills the grid split of sp (q, r or the weighted split, and the per-segment CTA
+// counts the tickets use)
+void split_grid(SegParams& sp, int grid, uint32_t split_cost = 0) {
   const uint64_t tw = sp.vstart[sp.nseg] >> 2, g = uint64_t(grid);
   const uint64_t units = (tw + kSplitWords - 1) / kSplitWords;
   sp.q = units / g;
   sp.r = units % g;
+  sp.units = units;
+  sp.split_cost = sp.nseg > 1 && grid <= kMaxSplitGrid ? split_cost : 0;
+  sp.lead_empty = 0;
+  for (int s = 1; s < sp.nseg && sp.vstart[s] == 0; ++s) ++sp.lead_empty;
+  if (sp.split_cost) {
+    const uint64_t total_cost = split_cost_at(sp, units);
+    sp.cq = total_cost / g;
+    sp.cr = uint32_t(total_cost % g);
+    std::vector<uint64_t> ub(g + 1);
+    for (uint32_t b = 0; b <= uint32_t(g); ++b) sp.cta_unit[b] = uint32_t(ub[b] = split_unit_of(sp, b, uint32_t(g)));
+    // CTAs with a non-empty range that meets segment s (units [first, last] of its words)
+    uint32_t b = 0;
+    for (int s = 0; s < sp.nseg; ++s) {
+      sp.ctas_after_first[s] = 0;
+      if (sp.vstart[s + 1] <= sp.vstart[s]) continue;
+      const uint64_t uf = (sp.vstart[s] >> 2) / kSplitWords, ul = ((sp.vstart[s + 1] >> 2) - 1) / kSplitWords;
+      while (ub[b + 1] <= uf) ++b;  // first CTA whose range reaches unit uf (ranges are monotone)
+      uint32_t n = 0;
+      for (uint32_t c = b; c < uint32_t(g) && ub[c] <= ul; ++c) n += ub[c + 1] > ub[c];
+      sp.ctas_after_first[s] = n - 1;
+    }
+    return;
+  }
   for (int s = 0; s < sp.nseg; ++s) {
     sp.ctas_after_first[s] = 0;
     if (sp.vstart[s + 1] > sp.vstart[s])
@@ -1105,7 +1184,7 @@ int launch_batch(const uint8_t* d_data, SegParams& sp, int kind, int impl, const
     const int per_sm = hot ? kLaneMinBlocks : kLaneBlocks;
     const int grid = int(std::max<uint64_t>(
         1, std::min<uint64_t>(want, uint64_t(di.sms) * per_sm - uint64_t(reserve_slots))));
-    split_grid(sp, grid);
+    split_grid(sp, grid, kLaneSplitCost);
     const int hb = pp ? pp->hot_bin : 0;
     // ADAPTIVE runs the register path for the pattern's hot bin only when the pattern
     // marks a dominant value (unique widest sub-bin run, and no HS_KIND_FLAG_SPREAD
