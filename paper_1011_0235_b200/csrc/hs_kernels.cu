@@ -1110,6 +1110,8 @@ uint32_t cta_of_word(uint64_t w, uint64_t tw, uint64_t g) {
 // 158.7 -> 157.0 us, 64 x 16 MiB 158.7 -> 158.3, 64 random sizes 161.2 -> 158.8; one
 // segment 156.7. The split is a host-computed table in the launch parameters: computing
 // it on the device (binary searches by thread 0 before the first load) cost 2 us.
+// Launches with several boundaries per CTA lose with it (256 x 1 MiB, 128 CTAs:
+// 49.6 -> 55.7 us), so it applies to full-grid launches with >= 2 CTAs per segment.
 #ifndef HS_SPLIT_COST
 #define HS_SPLIT_COST 32
 #endif
@@ -1184,7 +1186,11 @@ int launch_batch(const uint8_t* d_data, SegParams& sp, int kind, int impl, const
     const int per_sm = hot ? kLaneMinBlocks : kLaneBlocks;
     const int grid = int(std::max<uint64_t>(
         1, std::min<uint64_t>(want, uint64_t(di.sms) * per_sm - uint64_t(reserve_slots))));
-    split_grid(sp, grid, kLaneSplitCost);
+    // weighted split only for full-grid launches with at least two CTAs per segment:
+    // with several boundaries per CTA, or one CTA per SM, it measured slower
+    // (256 x 1 MiB: 49.6 -> 55.7 us)
+    const bool weighted = want == ~0ull && 2 * sp.nseg <= grid;
+    split_grid(sp, grid, weighted ? kLaneSplitCost : 0);
     const int hb = pp ? pp->hot_bin : 0;
     // ADAPTIVE runs the register path for the pattern's hot bin only when the pattern
     // marks a dominant value (unique widest sub-bin run, and no HS_KIND_FLAG_SPREAD

@@ -26,6 +26,10 @@ layouts = {}
 for k in (1, 16, 64, 256):
     b0 = np.arange(k, dtype=np.uint64) * (n // k)
     layouts[f"{k}x{(n // k) >> 20}MiB"] = (b0, b0 + np.uint64(n // k))
+b0 = np.arange(256, dtype=np.uint64) * (1 << 20)
+layouts["256x1MiB (256 MiB)"] = (b0, b0 + np.uint64(1 << 20))
+b0 = np.arange(64, dtype=np.uint64) * (1 << 20)
+layouts["64x1MiB (64 MiB)"] = (b0, b0 + np.uint64(1 << 20))
 cuts = np.sort(4 * rng.integers(1, n // 4, 63)).astype(np.uint64)
 layouts["64 random"] = (np.concatenate([[0], cuts]).astype(np.uint64), np.concatenate([cuts, [n]]).astype(np.uint64))
 line = [tag]
@@ -54,4 +58,6 @@ for name, (b0, b1) in layouts.items():
         b.synchronize()
         ts.append(a.elapsed_time(b) / 10 * 1e3)
     line.append(f"{name} {np.median(ts):6.1f}")
+    if k == 256 and name.startswith("256x1"):
+        line[-1] += f" ({np.median(ts) / 256:.3f}/seg)"
 print(" | ".join(line), flush=True)
