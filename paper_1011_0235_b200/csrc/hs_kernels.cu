@@ -1132,8 +1132,8 @@ void split_grid(SegParams& sp, int grid, uint32_t split_cost = 0) {
     const uint64_t total_cost = split_cost_at(sp, units);
     sp.cq = total_cost / g;
     sp.cr = uint32_t(total_cost % g);
-    std::vector<uint64_t> ub(g + 1);
-    for (uint32_t b = 0; b <= uint32_t(g); ++b) sp.cta_unit[b] = uint32_t(ub[b] = split_unit_of(sp, b, uint32_t(g)));
+    uint32_t* ub = sp.cta_unit;  // units of one launch (<= 1 GiB) fit 32 bits
+    for (uint32_t b = 0; b <= uint32_t(g); ++b) ub[b] = uint32_t(split_unit_of(sp, b, uint32_t(g)));
     // CTAs with a non-empty range that meets segment s (units [first, last] of its words)
     uint32_t b = 0;
     for (int s = 0; s < sp.nseg; ++s) {
