@@ -387,13 +387,20 @@ def histograms(chunks: Sequence, kind: int, pattern=None, impl: int = N.HS_IMPL_
     return readback(out, st, stream)
 
 
+def _raw_stream(index: int) -> int:
+    """The current stream's handle on device ``index`` (torch's raw accessor skips the
+    Stream object; public API otherwise)."""
+    t = torch()
+    raw = getattr(t._C, "_cuda_getCurrentRawStream", None)
+    return raw(index) if raw is not None else t.cuda.current_stream(index).cuda_stream
+
+
 def _one_histogram(chunk, kind, pattern, impl, st: "Staging") -> np.ndarray:
     """One chunk (the per-image path of naive_histogram / adaptive_histogram) through
     the blocking native entries with arguments prepared once per staging: on a
     1024x1024 image, marshalling the arguments anew each call cost as much as the
     launch, kernel, readback and wait together (tools/c1_breakdown.py)."""
-    t = torch()
-    stream = t._C._cuda_getCurrentRawStream(st.device.index)
+    stream = _raw_stream(st.device.index)
     kind = int(_with_hints(kind, pattern))
     if type(chunk) is DeviceChunk:
         one = st.one_call()
