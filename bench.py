@@ -431,6 +431,9 @@ def main(argv=None):
     for j in range(len(SIGMAS)):
         got = outs[j][par[0] ^ 1].sum().item()
         assert got == GiB, f"stream {j}: counted {got} != {GiB}"
+        for c in (0, 37, 63):  # and bit-exact per chunk against a host count
+            want = np.bincount(streams[j][c * CHUNK:(c + 1) * CHUNK].cpu().numpy(), minlength=256)
+            assert np.array_equal(outs[j][par[0] ^ 1][c].cpu().numpy(), want), f"stream {j} chunk {c}"
     if dist_on:
         assert int(total_counts[par[0] ^ 1].sum().item()) == world * len(SIGMAS) * GiB, "allreduced total"
 
