@@ -67,7 +67,8 @@ struct SegParams {
   // whose range crosses a segment boundary flushes its counters there (barrier, drain
   // of the load pipeline, 256 global REDs), so such a CTA is given split_cost fewer
   // units. Cost(u) = u + split_cost * (boundaries before unit u); CTA b starts at the
-  // first unit whose cost reaches floor(b * Cost(units) / grid) = cq*b + cr*b/grid.
+  // first unit whose cost reaches floor(b * Cost(units) / grid) = cq*b + cr*b/grid,
+  // tabulated on the host in cta_unit (the fields above it describe the split).
   uint32_t split_cost;
   uint32_t lead_empty;           // boundaries s >= 1 at virtual offset 0 (not counted)
   uint64_t units;                // kSplitWords units of the launch
@@ -77,8 +78,8 @@ struct SegParams {
   uint32_t cta_unit[kMaxSplitGrid + 1];  // weighted split: first unit of CTA b (host-computed)
 };
 
-// Cost of the first u units under the weighted split (host and device)
-__host__ __device__ __forceinline__ uint64_t split_cost_at(const SegParams& sp, uint64_t u) {
+// Cost of the first u units under the weighted split (host: the table is built at launch)
+inline uint64_t split_cost_at(const SegParams& sp, uint64_t u) {
   const uint64_t x = u * (4 * kSplitWords);
   int lo = 1, hi = sp.nseg;  // first s in [1, nseg) with vstart[s] >= x
   while (lo < hi) {
@@ -91,8 +92,8 @@ __host__ __device__ __forceinline__ uint64_t split_cost_at(const SegParams& sp, 
 }
 
 // First unit of CTA b (b == grid: the end) under the weighted split
-__host__ __device__ __forceinline__ uint64_t split_unit_of(const SegParams& sp, uint32_t b, uint32_t grid) {
-  const uint64_t t = sp.cq * b + (sp.cr * b) / grid;  // cr < grid <= a few thousand: 32-bit
+inline uint64_t split_unit_of(const SegParams& sp, uint32_t b, uint32_t grid) {
+  const uint64_t t = sp.cq * b + (uint64_t(sp.cr) * b) / grid;
   uint64_t lo = 0, hi = sp.units;
   while (lo < hi) {
     const uint64_t mid = (lo + hi) >> 1;
