@@ -142,6 +142,21 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------- distributed
+def relaunch_under_torchrun(n: int, argv) -> int:
+    """`python bench.py --gpus N` without a launcher: re-run under torch.distributed.run
+    with one process per GPU (rendezvous on 127.0.0.1), as the driver launches it."""
+    import socket
+    import subprocess
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()),
+           *(sys.argv[1:] if argv is None else argv)]
+    return subprocess.call(cmd)
+
+
 def dist_setup(args):
     """One process per GPU. Under torchrun (RANK set) NCCL is initialised even at
     world size 1, so the collective code path is the one that runs."""
@@ -266,6 +281,8 @@ def main(argv=None):
     ap.add_argument("--no-extras", action="store_true")
     args = ap.parse_args(argv)
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "RANK" not in os.environ:
+        return relaunch_under_torchrun(args.gpus, argv)
     if args.impl == "reference":
         return run_reference(args)
 
