@@ -38,7 +38,7 @@
 
 namespace {
 
-constexpr int kMaxSeg = 256;         // segments per launch (SegParams ~5 KB: large kernel params)
+constexpr int kMaxSeg = 256;         // segments per launch (SegParams ~6.5 KB: large kernel params)
 constexpr int kMaxSegEngine = 64;    // per hs_stream_step batch (the fold stages it in shared memory)
 constexpr size_t kTicketBytes = 1024;  // workspace head: kMaxSeg u32 tickets
 constexpr uint64_t kBigCap = 1ull << 30;  // u32 per-warp counters: far from wrapping
