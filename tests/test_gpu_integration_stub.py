@@ -35,3 +35,18 @@ def test_documented_stub_counts_exactly(cuda, oracle):
     pattern = hs.compute_binning_pattern(hs.Histogram256(want[1]))
     got = stub["batch_on_b200"](chunks, True, pattern)
     assert [g.counts.tolist() for g in got] == [w.tolist() for w in want]
+
+
+def test_plain_c_host_counts_exactly(cuda, tmp_path):
+    """examples/c_api_demo.c: the C ABI from a C program with no Python or torch in the
+    process (cudaMalloc'd buffers, batched NAIVE and ADAPTIVE, host control plane,
+    blocking host entry), each result checked against a host count inside the demo."""
+    import subprocess
+    import sys
+
+    sys.path.insert(0, str(Path(__file__).resolve().parent))
+    from test_native_abi import _build_c_demo
+
+    exe = _build_c_demo(tmp_path)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and "c_api_demo ok" in r.stdout, r.stdout + r.stderr

@@ -158,3 +158,30 @@ def test_sync_entry_points_validate_first():
                                  None) == N.HS_ERR_INVALID_ARG
     assert lib.hs_histogram_sync(p, N.u64p(b), N.u64p(e), 1, 7, 0, None, None, 0, 0, p, N.u64p(h_out), None, 0,
                                  None) == N.HS_ERR_INVALID_ARG
+
+
+def _build_c_demo(tmp_path):
+    """Compile examples/c_api_demo.c (plain C against include/hist256.h, linked with
+    libhist256.so and the CUDA runtime) into tmp_path."""
+    import shutil
+    import subprocess
+
+    root = Path(__file__).resolve().parents[1]
+    exe = tmp_path / "c_api_demo"
+    cuda = Path("/usr/local/cuda")
+    cmd = ["gcc", "-O2", "-std=c11", "-Wall", "-Wextra", "-Werror", "-I", str(root / "include"),
+           "-I", str(cuda / "include"), str(root / "examples" / "c_api_demo.c"),
+           "-L", str(N.library_path().parent), "-lhist256", "-L", str(cuda / "lib64"), "-lcudart",
+           f"-Wl,-rpath,{N.library_path().parent}", f"-Wl,-rpath,{cuda / 'lib64'}", "-o", str(exe)]
+    if shutil.which("gcc") is None:
+        import pytest
+
+        pytest.skip("gcc not available")
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    return exe
+
+
+def test_c_demo_compiles_against_the_header(tmp_path):
+    """The ABI is usable from plain C: the demo builds with -Wall -Wextra -Werror."""
+    assert _build_c_demo(tmp_path).exists()
