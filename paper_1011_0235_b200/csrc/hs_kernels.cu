@@ -5,7 +5,8 @@
 //   _naive_worker     kernels.py:97-130   -> k_lane (HS_IMPL_LANE) / k_warp (HS_IMPL_WARP)
 //   _adaptive_worker  kernels.py:133-168  -> k_lane<HOT> (HS_IMPL_LANE) / k_subbin (HS_IMPL_SUBBIN)
 //   reduce_subbins    kernels.py:410-418  -> fused flush epilogues below
-//   merge_all         core.py:152-156     -> u64 RED into d_out (integer adds commute: exact)
+//   merge_all         core.py:152-156     -> u64 RED into a workspace row per segment, moved to d_out by
+//                                            the segment's last CTA (integer adds commute: exact)
 //   batch_histograms  stream.py:260-316   -> one launch per <= kMaxSeg segments and <= 1 GiB
 //   _adaptive_worker_traced / _u16        -> k_group_slots (reference group/lane mapping)
 //   _stage_*_worker   kernels.py:212-264  -> k_ablation
@@ -26,6 +27,11 @@
 //   * Launches are chained with programmatic dependent launch (griddepcontrol): a launch
 //     streams while the previous one's tail drains and waits only before its first
 //     global write. Output is ticketed: one kernel per launch, no memset.
+//   * CTA ranges are whole 4 KiB units of the launch's concatenated range; full-grid
+//     launches over several segments weight the split so that a CTA crossing a segment
+//     boundary (and paying a flush there) gets less data.
+//   * The blocking entries (hs_histogram_sync / hs_histogram_host) size the grid for
+//     latency and let the kernel write the counts into a page-locked h_out.
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdlib>
