@@ -142,20 +142,23 @@ def test_split_launches_over_groups(cuda, oracle):
 def test_weighted_split_random_layouts(cuda, seed):
     """Full-grid launches with <= 148 segments take the cost-weighted CTA split (a CTA
     that crosses a segment boundary gets fewer units). Random word-multiple segment
-    sizes over 1.5 GiB (some empty, some a few words, one crossing the 1 GiB launch
-    cut), NAIVE and the register (HOT) form, against torch.bincount per segment; the
-    workspace must be zero again afterwards."""
+    sizes over 1.5 GiB (some empty, one crossing the 1 GiB launch cut) at a base 0, 4
+    or 8 bytes past a 16-B boundary, NAIVE and the register (HOT) form, against
+    torch.bincount per segment; the workspace must be zero again afterwards."""
     torch = cuda
     rng = np.random.default_rng(77 + seed)
     n = 3 * GiB // 2
+    off = 4 * seed
     buf = torch.empty(n, dtype=torch.uint8, device="cuda")
     hs.generate_device(hs.SourceSpec("normal", n, seed, mean=60.0, sigma=5.0), buf)
+    span = n - 16
     nseg = int(rng.integers(2, 140))
-    cuts = np.sort(4 * rng.integers(0, n // 4, nseg - 1))
+    cuts = np.sort(4 * rng.integers(0, span // 4, nseg - 1))
     cuts[: max(1, nseg // 10)] = cuts[0]  # a run of empty segments
     b0 = np.concatenate([[0], cuts]).astype(np.uint64)
-    b1 = np.concatenate([cuts, [n]]).astype(np.uint64)
-    want = np.stack([torch.bincount(buf[int(a):int(b)], minlength=256).cpu().numpy() for a, b in zip(b0, b1)])
+    b1 = np.concatenate([cuts, [span]]).astype(np.uint64)
+    want = np.stack([torch.bincount(buf[off + int(a):off + int(b)], minlength=256).cpu().numpy()
+                     for a, b in zip(b0, b1)])
     L = N.lib()
     ws = torch.zeros(int(L.hs_workspace_bytes(256)), dtype=torch.uint8, device="cuda")
     deg = np.zeros(256, np.uint64)
@@ -163,7 +166,7 @@ def test_weighted_split_random_layouts(cuda, seed):
     hot = hs.compute_binning_pattern(hs.Histogram256(deg))
     for kind, p in ((N.HS_KIND_NAIVE, None), (N.HS_KIND_ADAPTIVE, hot)):
         out = torch.full((nseg, 256), -1, dtype=torch.int64, device="cuda")
-        N.check(L.hs_histogram_batched(buf.data_ptr(), N.u64p(b0), N.u64p(b1), nseg, kind, N.HS_IMPL_AUTO,
+        N.check(L.hs_histogram_batched(buf.data_ptr() + off, N.u64p(b0), N.u64p(b1), nseg, kind, N.HS_IMPL_AUTO,
                                        N.i64p(p.offset) if p else None, N.i64p(p.count) if p else None,
                                        960 if p else 0, 8 if p else 0, out.data_ptr(), ws.data_ptr(), ws.numel(),
                                        torch.cuda.current_stream().cuda_stream), "weighted")
