@@ -51,10 +51,11 @@ WORKLOAD = "xray-normal-stream: 3 x 1 GiB (sigma 8/32/64, mean 128) in 16 MiB ch
 
 def peaks():
     p = ROOT / "MEASURED_PEAKS.json"
-    if p.exists():
+    try:
         d = json.loads(p.read_text())
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
-    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+    except (OSError, ValueError, KeyError, TypeError):
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
 def host_cores() -> int:
