@@ -291,3 +291,23 @@ def test_bench_helpers():
             assert B.median(xs) == R.median(xs) and B.relative_spread(xs) == R.relative_spread(xs), n
         for a, b in ((1.0, 1.0), (1.11, 1.0), (1.0, 1.11), (2.0, 1.0)):
             assert B.ordering(a, b).value == R.ordering(a, b).value
+
+
+def test_bench_relaunches_itself_under_torchrun(monkeypatch):
+    """`python bench.py --gpus N` without a launcher re-runs under torch.distributed.run
+    with N processes and a 127.0.0.1 rendezvous, passing the arguments through."""
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    import bench
+
+    seen = {}
+    monkeypatch.delenv("RANK", raising=False)
+    monkeypatch.setattr(subprocess, "call", lambda cmd: seen.setdefault("cmd", cmd) and 0)
+    assert bench.main(["--gpus", "4", "--steps", "7", "--warmup", "3"]) == 0
+    cmd = seen["cmd"]
+    assert cmd[1:3] == ["-m", "torch.distributed.run"] and "--nproc-per-node=4" in cmd
+    assert cmd[cmd.index("--master-addr") + 1] == "127.0.0.1"
+    assert cmd[-6:] == ["--gpus", "4", "--steps", "7", "--warmup", "3"]
