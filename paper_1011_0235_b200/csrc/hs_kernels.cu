@@ -1365,7 +1365,8 @@ int histogram_batched(const uint8_t* d_data, const uint64_t* h_begin, const uint
   }
   uint64_t total = 0;
   for (int s = 0; s < nseg; ++s) {
-    if ((h_begin[s] & 3) || (h_end[s] & 3) || h_end[s] < h_begin[s]) return HS_ERR_ALIGNMENT;
+    if (h_end[s] < h_begin[s]) return HS_ERR_INVALID_ARG;
+    if ((h_begin[s] & 3) || (h_end[s] & 3)) return HS_ERR_ALIGNMENT;
     total += h_end[s] - h_begin[s];
   }
   if (total > 0 && !d_data) return HS_ERR_INVALID_ARG;
@@ -1600,7 +1601,8 @@ int hs_stream_step(const uint8_t* d_data, const uint64_t* h_begin, const uint64_
   if (!d_ws || ws_bytes < kWorkspaceBytes) return HS_ERR_WORKSPACE;
   uint64_t total = 0;
   for (int s = 0; s < nseg; ++s) {
-    if ((h_begin[s] & 3) || (h_end[s] & 3) || h_end[s] < h_begin[s]) return HS_ERR_ALIGNMENT;
+    if (h_end[s] < h_begin[s]) return HS_ERR_INVALID_ARG;
+    if ((h_begin[s] & 3) || (h_end[s] & 3)) return HS_ERR_ALIGNMENT;
     total += h_end[s] - h_begin[s];
   }
   if (reinterpret_cast<uintptr_t>(d_data) & 3) return HS_ERR_ALIGNMENT;

@@ -58,6 +58,8 @@ def test_argument_validation_before_device_work():
     # misaligned segment bounds
     e3 = np.full(1, 6, np.uint64)
     assert lib.hs_histogram_batched(ctypes.c_void_p(256), N.u64p(b), N.u64p(e3), 1, 0, 0, None, None, 0, 0, out, None, 0, None) == N.HS_ERR_ALIGNMENT
+    # a segment that ends before it begins
+    assert lib.hs_histogram_batched(ctypes.c_void_p(256), N.u64p(e), N.u64p(b), 1, 0, 0, None, None, 0, 0, out, None, 0, None) == N.HS_ERR_INVALID_ARG
     # invalid patterns, in the reference's check order
     off = np.arange(256, dtype=np.int64) * 3
     cnt = np.full(256, 3, np.int64)
