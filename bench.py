@@ -499,6 +499,7 @@ def main(argv=None):
                 # streaming kernel (tools/microbench/spread.cu, grid-stride, 64 GiB) reaches
                 # this on the same boxes, the ceiling for a 1-byte-read-per-pixel kernel
                 "read_only_ceiling_gbs": READ_ONLY_CEILING_GBS,
+                "frac_of_read_only_ceiling": round(achieved / READ_ONLY_CEILING_GBS, 4),
                 "achieved_method": "1 GiB / mean launch duration (CUDA events around 10 back-to-back launches per sigma stream, after warm-up, before the timed region)",
                 "concurrent_streams_gbs": round(value / world, 1),
                 "kernel": "k_lane, kind ADAPTIVE (hs_histogram_batched, 64 x 16 MiB segments)",
