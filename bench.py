@@ -330,32 +330,45 @@ def main(argv=None):
     wss = [torch.zeros(int(L.hs_workspace_bytes(64)), dtype=torch.uint8, device=dev) for _ in SIGMAS]
     dist_on = _dist_on()
 
+    # per-launch host work is the path's own (lag-1 pattern on the host) plus argument
+    # marshalling; the marshalling is done once here so the host stays ahead of the GPU
+    b_p, e_p = N.u64p(begin), N.u64p(end)
+    data_p = [t.data_ptr() for t in streams]
+    out_p = [[outs[j][k].data_ptr() for k in range(2)] for j in range(len(SIGMAS))]
+    ws_p = [(w.data_ptr(), w.numel()) for w in wss]
+    side_h = [sj.cuda_stream for sj in side]
+    host_np = [[host[j][k].numpy().view(np.uint64) for k in range(2)] for j in range(len(SIGMAS))]
+    done_ev = [[torch.cuda.Event() for _ in range(2)] for _ in SIGMAS]  # reused by parity
+    pat_args = [None] * len(SIGMAS)
+
     def launch(j):
         # lag-1 pattern for stream j: its previous step's per-chunk histograms, read back
         # asynchronously while the other streams' kernels ran
         if j in pending:
-            ev, hb = pending.pop(j)
+            ev, k = pending.pop(j)
             w0 = time.perf_counter()
             ev.synchronize()
             host_wait[0] += time.perf_counter() - w0
-            prior = hb.numpy().view(np.uint64).sum(axis=0, dtype=np.uint64)
+            prior = host_np[j][k].sum(axis=0, dtype=np.uint64)
             patterns[j] = hs.compute_binning_pattern(hs.Histogram256(prior))
+            pat_args[j] = None
         p = patterns[j]
+        if pat_args[j] is None:
+            pat_args[j] = (D._with_hints(N.HS_KIND_ADAPTIVE, p), N.i64p(p.offset), N.i64p(p.count))
+        kind, off_p, cnt_p = pat_args[j]
         sj = side[j]
-        o = outs[j][par[0]]
         if red_done[par[0]] is not None:
             sj.wait_event(red_done[par[0]])  # the allreduce two steps back has read o
-        st = L.hs_histogram_batched(streams[j].data_ptr(), N.u64p(begin), N.u64p(end), 64, N.HS_KIND_ADAPTIVE,
-                                    N.HS_IMPL_AUTO, N.i64p(p.offset), N.i64p(p.count), 960, 8,
-                                    o.data_ptr(), wss[j].data_ptr(), wss[j].numel(), sj.cuda_stream)
+        st = L.hs_histogram_batched(data_p[j], b_p, e_p, 64, kind, N.HS_IMPL_AUTO, off_p, cnt_p, 960, 8,
+                                    out_p[j][par[0]], ws_p[j][0], ws_p[j][1], side_h[j])
         N.check(st, "hs_histogram_batched")
-        hb = host[j][flip[j]]
+        k = flip[j]
         flip[j] ^= 1
         with torch.cuda.stream(sj):
-            hb.copy_(o, non_blocking=True)
-        ev = torch.cuda.Event()
+            host[j][k].copy_(outs[j][par[0]], non_blocking=True)
+        ev = done_ev[j][k]
         ev.record(sj)
-        pending[j] = (ev, hb)
+        pending[j] = (ev, k)
 
     def step():
         for j in range(len(SIGMAS)):
