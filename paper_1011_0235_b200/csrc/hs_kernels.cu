@@ -34,6 +34,9 @@
 //     latency and let the kernel write the counts into a page-locked h_out.
 #include <cuda_runtime.h>
 #include <cstdint>
+#ifdef HS_CHECK_SPLIT
+#include <cstdio>
+#endif
 #include <cstdlib>
 #include <cstring>
 #include <algorithm>
@@ -97,7 +100,9 @@ inline uint64_t split_cost_at(const SegParams& sp, uint64_t u) {
   return u + uint64_t(sp.split_cost) * nb;
 }
 
-// First unit of CTA b (b == grid: the end) under the weighted split
+#ifdef HS_CHECK_SPLIT
+// First unit of CTA b (b == grid: the end) under the weighted split, by binary search:
+// the definition split_table() is checked against in HS_CHECK_SPLIT builds
 inline uint64_t split_unit_of(const SegParams& sp, uint32_t b, uint32_t grid) {
   const uint64_t t = sp.cq * b + (uint64_t(sp.cr) * b) / grid;
   uint64_t lo = 0, hi = sp.units;
@@ -107,6 +112,7 @@ inline uint64_t split_unit_of(const SegParams& sp, uint32_t b, uint32_t grid) {
   }
   return lo;
 }
+#endif
 
 struct PatternParams {
   uint32_t entry[256];           // offset | count << 16   (sub-bin kernels)
@@ -1124,6 +1130,32 @@ uint32_t cta_of_word(uint64_t w, uint64_t tw, uint64_t g) {
 #endif
 constexpr uint32_t kLaneSplitCost = HS_SPLIT_COST;
 
+// The weighted split's table in one pass: CTA targets rise with b, so the first unit
+// whose cost reaches each target is found by walking units and boundaries forward
+// (O(grid + nseg); split_unit_of's binary searches were ~30 us per launch on the host).
+// Boundary s counts from unit vstart[s] / unit_bytes + 1 on (Cost counts vstart < u*unit).
+void split_table(const SegParams& sp, uint32_t g, uint32_t* ub) {
+  const uint64_t unit_bytes = 4 * kSplitWords, d = sp.split_cost;
+  int k = 1 + int(sp.lead_empty);
+  uint64_t u = 0, nb = 0;
+  for (uint32_t b = 0; b <= g; ++b) {
+    const uint64_t t = sp.cq * b + (uint64_t(sp.cr) * b) / g;
+    for (;;) {
+      const uint64_t jump = k < sp.nseg ? sp.vstart[k] / unit_bytes + 1 : ~0ull;
+      const uint64_t need = t > d * nb ? t - d * nb : 0;
+      const uint64_t cand = std::max(u, need);
+      if (cand < jump) {
+        u = cand;
+        break;
+      }
+      u = jump;  // no unit before the boundary reaches t: cross it
+      ++nb;
+      ++k;
+    }
+    ub[b] = uint32_t(u);
+  }
+}
+
 // fills the grid split of sp (q, r or the weighted split, and the per-segment CTA
 // counts the tickets use)
 void split_grid(SegParams& sp, int grid, uint32_t split_cost = 0) {
@@ -1140,7 +1172,14 @@ void split_grid(SegParams& sp, int grid, uint32_t split_cost = 0) {
     sp.cq = total_cost / g;
     sp.cr = uint32_t(total_cost % g);
     uint32_t* ub = sp.cta_unit;  // units of one launch (<= 1 GiB) fit 32 bits
-    for (uint32_t b = 0; b <= uint32_t(g); ++b) ub[b] = uint32_t(split_unit_of(sp, b, uint32_t(g)));
+    split_table(sp, uint32_t(g), ub);
+#ifdef HS_CHECK_SPLIT
+    for (uint32_t b = 0; b <= uint32_t(g); ++b)
+      if (ub[b] != split_unit_of(sp, b, uint32_t(g))) {
+        fprintf(stderr, "[hs] split table mismatch at CTA %u\n", b);
+        abort();
+      }
+#endif
     // CTAs with a non-empty range that meets segment s (units [first, last] of its words)
     uint32_t b = 0;
     for (int s = 0; s < sp.nseg; ++s) {
