@@ -55,6 +55,20 @@ extern "C" {
  * dominated by one value (max-bin share below ~0.999), so the register path for the hot
  * bin would not pay and the plain lane core runs. Counts are identical either way. */
 #define HS_KIND_FLAG_SPREAD 0x100
+/* OR-ed into kind: the caller guarantees that the kernel preceding this call on the
+ * stream is a libhist256 launch (for instance the previous call over the same resident
+ * input) and that the input was complete before that launch was issued. The call's
+ * first launch may then start streaming before its predecessor finishes (programmatic
+ * dependent launch). Without it the first launch waits for its predecessor before its
+ * first load, so input written by ANY preceding kernel -- including producers that
+ * trigger their dependents early -- is read only once complete. */
+#define HS_KIND_FLAG_CHAINED 0x200
+/* OR-ed into kind: merge every segment into ONE histogram, d_out = uint64[256] = the
+ * sum over all nseg segments (merge_all of the per-slice histograms, core.py:152-156),
+ * formed in the kernel epilogue: CTAs do not flush at segment boundaries, and with a
+ * workspace one ticket per CTA finalizes the row. A rank's partial for the multi-GPU
+ * path (one call over its shard, then one allreduce of 256 counts). */
+#define HS_KIND_FLAG_MERGE 0x400
 
 /* ---- device strategies behind a kind --------------------- */
 #define HS_IMPL_AUTO 0       /* library picks by kind and size                     */
@@ -97,7 +111,7 @@ size_t hs_workspace_bytes(int nseg);
  *   impl     HS_IMPL_* (HS_IMPL_AUTO for production)
  *   h_offset/h_count: the CPU binning pattern (pattern.py:94-133), may be NULL
  *            for NAIVE; validated before launch (kernels.py:363).
- *   d_out    uint64[nseg*256], overwritten.
+ *   d_out    uint64[nseg*256] (uint64[256] with HS_KIND_FLAG_MERGE), overwritten.
  *   d_ws     optional workspace of hs_workspace_bytes() bytes, zeroed once by the caller:
  *            the call is then ONE kernel launch per <= 256 segments and 1 GiB (CTAs RED into
  *            workspace rows; the last CTA per segment stores d_out and re-zeroes its row).
@@ -154,10 +168,13 @@ int hs_histogram(const uint8_t* d_data, uint64_t n_bytes, int kind, int impl,
  *   mode 1: d_out uint64[group_count][group_size][total_slots] (lane_touch)
  *   mode 2: d_out uint16[group_count][total_slots], each slot wrapped mod 2^16
  *           (_adaptive_worker_u16, kernels.py:267-303)
- * d_out is overwritten. Intended for test-scale inputs (global atomics). */
+ * d_out is overwritten. Mode 2 needs a device workspace of hs_group_slots_ws_bytes()
+ * bytes (exact totals before the wrap; contents on entry do not matter); modes 0/1 need
+ * none (d_ws may be NULL). Intended for test-scale inputs (global atomics). */
+size_t hs_group_slots_ws_bytes(int group_size, int group_count, int64_t total_slots, int mode);
 int hs_group_slots(const uint8_t* d_data, uint64_t n_bytes, int group_size, int group_count,
                    const int64_t* h_offset, const int64_t* h_count, int64_t total_slots,
-                   int64_t cap, int mode, void* d_out, void* stream);
+                   int64_t cap, int mode, void* d_out, void* d_ws, size_t ws_bytes, void* stream);
 
 /* Genealogy ablation stage (run_ablation, kernels.py:421-496) on the sub-bin kernel
  * skeleton. d_sink: uint64[1] checksum; d_out256 receives the histogram for
@@ -181,6 +198,10 @@ size_t hs_stream_state_bytes(int window_size);
 int hs_stream_reset(void* d_state, int window_size, void* stream);
 
 /* One iteration: histograms of the batch's nseg (<= 64) segments into d_out[nseg][256],
+ * Input contract: the histogram launch is chained behind the previous step's fold (or
+ * hs_stream_reset) with programmatic dependent launch and reads the batch before that
+ * predecessor has finished, so the batch's bytes must be complete before the previous
+ * step was issued (produced ahead, or ordered before the stream's previous step).
  * then the fold: acc += each chunk, window push/evict (error bit on NegativeCount),
  * d_kind_log[iteration] = kind the previous fold decided, d_deg_log[iteration] = window
  * degeneracy,

@@ -71,6 +71,24 @@ def histogram(pixels: np.ndarray) -> np.ndarray:
     return out
 
 
+def histogram_mt(pixels: np.ndarray, threads: int | None = None, piece: int = 64 << 20) -> np.ndarray:
+    """reference_histogram over a large pixel stream with host threads: the C count of
+    each piece (ctypes releases the GIL) and the componentwise sum of the partials
+    (merge_all, core.py:152-156). For multi-GiB parity checks."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+
+    p = np.ascontiguousarray(pixels, dtype=np.uint8).reshape(-1)
+    threads = threads or len(os.sched_getaffinity(0))
+    cuts = list(range(0, p.size, piece)) + [p.size]
+    with ThreadPoolExecutor(max(1, threads)) as ex:
+        parts = list(ex.map(lambda ab: histogram(p[ab[0]:ab[1]]), zip(cuts, cuts[1:])))
+    out = np.zeros(BINS, np.uint64)
+    for h in parts:
+        out += h
+    return out
+
+
 def group_ranges(word_count: int, group_count: int) -> list[tuple[int, int]]:
     """kernels.py:311-316 (the C restatement, returned as Python tuples)."""
     st = np.zeros(group_count, np.int64)

@@ -36,6 +36,8 @@ HS_ERR_CUDA_BASE = -1000
 HS_KIND_NAIVE = 0
 HS_KIND_ADAPTIVE = 1
 HS_KIND_FLAG_SPREAD = 0x100
+HS_KIND_FLAG_CHAINED = 0x200
+HS_KIND_FLAG_MERGE = 0x400
 
 HS_IMPL_AUTO = 0
 HS_IMPL_LANE = 1
@@ -65,6 +67,7 @@ EXPORTED = (
     "hs_histogram_host",
     "hs_histogram_sync",
     "hs_histogram",
+    "hs_group_slots_ws_bytes",
     "hs_group_slots",
     "hs_ablation_stage",
     "hs_binning_pattern",
@@ -106,9 +109,10 @@ _SIGNATURES = {
         _c.c_int,
         [_P, _U64, _c.c_int, _c.c_int, _I64P, _I64P, _I64, _I64, _P, _P, _c.c_size_t, _P],
     ),
+    "hs_group_slots_ws_bytes": (_c.c_size_t, [_c.c_int, _c.c_int, _I64, _c.c_int]),
     "hs_group_slots": (
         _c.c_int,
-        [_P, _U64, _c.c_int, _c.c_int, _I64P, _I64P, _I64, _I64, _c.c_int, _P, _P],
+        [_P, _U64, _c.c_int, _c.c_int, _I64P, _I64P, _I64, _I64, _c.c_int, _P, _P, _c.c_size_t, _P],
     ),
     "hs_ablation_stage": (
         _c.c_int,

@@ -85,7 +85,17 @@ struct SegParams {
   uint32_t cr;
   uint32_t ctas_after_first[kMaxSeg];  // CTAs with work in segment s, minus one
   uint32_t cta_unit[kMaxSplitGrid + 1];  // weighted split: first unit of CTA b (host-computed)
+  // HS_KIND_FLAG_MERGE: every segment counts into ONE output row (merge_all of the
+  // per-slice histograms, core.py:152-156, formed in the epilogue): a CTA flushes once
+  // whatever the segment boundaries in its range, and only the call's last launch
+  // (merge_final) takes tickets -- merge_ctas + 1 of its CTAs have work.
+  int merge;
+  int merge_final;
+  uint32_t merge_ctas;
 };
+
+// output / accumulator row of launch-local segment s
+__host__ __device__ __forceinline__ int seg_row(const SegParams& sp, int s) { return sp.merge ? 0 : s; }
 
 // Cost of the first u units under the weighted split (host: the table is built at launch)
 inline uint64_t split_cost_at(const SegParams& sp, uint64_t u) {
@@ -378,10 +388,15 @@ __device__ __forceinline__ void lane_tickets(const Tickets& tk, const SegParams&
                                           unsigned long long* __restrict__ out) {
   __shared__ int last_seg[kMaxSeg];
   __shared__ int n_last;
+  if (sp.merge && !sp.merge_final) return;  // a later launch of the call finalizes the row
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
     int m = 0;
+    if (sp.merge) {
+      if (atomicAdd(tk.ticket + sp.acc_base, 1u) == sp.merge_ctas) last_seg[m++] = 0;
+      s_last = -1;  // no per-segment tickets
+    }
     for (int s = s_first; s <= s_last; ++s) {
       if (sp.vstart[s + 1] == sp.vstart[s]) continue;  // empty: no CTA owns it
       if ((sp.open_mask[s >> 5] >> (s & 31)) & 1) continue;  // finalized by a later launch
@@ -490,10 +505,16 @@ __device__ __forceinline__ uint32_t lane_piece(const uint8_t* __restrict__ data,
 }
 
 // HOT (ADAPTIVE): register path for the hot bin `hot_bin`.
+// wait_first: the first launch of a public call, whose stream predecessor may be the
+// kernel that wrote the input: wait for it before the first load and only then let
+// the next launch start (so a chained launch after us never overtakes that producer).
+// Chained launches (later launches of the same call, hs_stream_step, or a caller's
+// HS_KIND_FLAG_CHAINED) stream before their predecessor -- a libhist256 kernel, which
+// never writes the input -- has finished, and wait only before their first write.
 template <int U, bool HOT, int TH = kLaneThreads, int MB = kLaneBlocks>
 __global__ void __launch_bounds__(TH, MB)
     k_lane(const uint8_t* __restrict__ data, const __grid_constant__ SegParams sp, int hot_bin,
-           unsigned long long* __restrict__ out, Tickets tk) {
+           unsigned long long* __restrict__ out, Tickets tk, int wait_first) {
   __shared__ __align__(16) uint32_t counters[256 * 32];
   // The CTA's pieces (segment, byte range) are listed in shared memory first, so no
   // segment-walk state is live across the streaming loop (it would take registers the
@@ -502,6 +523,7 @@ __global__ void __launch_bounds__(TH, MB)
   __shared__ int pc_seg[kMaxSeg];
   __shared__ int pc_n;
   HS_STAMP(0);
+  if (wait_first) pdl_wait();
   pdl_launch_dependents();  // the next launch's CTAs may take SMs as ours retire
   if (threadIdx.x == 0) {
     int n = 0;
@@ -518,7 +540,7 @@ __global__ void __launch_bounds__(TH, MB)
   __syncthreads();
   const uint32_t tb = sbase + (threadIdx.x & 31) * 4;  // column base: bank == lane
   const uint32_t hot = uint32_t(hot_bin) & 0xff;
-  if (tk.ticket != nullptr && blockIdx.x == 0) {
+  if (tk.ticket != nullptr && blockIdx.x == 0 && !sp.merge) {
     // ticketed launches have no memset: CTA 0 zeroes the empty segments' outputs
     bool any_empty = false;
     for (int s = 0; s < sp.nseg; ++s) any_empty |= sp.vstart[s + 1] == sp.vstart[s];
@@ -537,8 +559,9 @@ __global__ void __launch_bounds__(TH, MB)
   for (int i = 0; i < pc_n; ++i) {
     lane_piece<U, HOT, TH>(data, pc_p0[i], pc_p1[i], tb, hot4);
     HS_STAMP(2 + 2 * i);
-    const int s = pc_seg[i];
-    lane_flush(sbase, ticketed ? tk.acc + size_t(sp.acc_base + s) * 256 : out + size_t(sp.out_base + s) * 256,
+    if (sp.merge && i + 1 < pc_n) continue;  // merged output: one flush per CTA
+    const int r = seg_row(sp, pc_seg[i]);
+    lane_flush(sbase, ticketed ? tk.acc + size_t(sp.acc_base + r) * 256 : out + size_t(sp.out_base + r) * 256,
                i + 1 < pc_n);
     HS_STAMP(3 + 2 * i);
   }
@@ -573,7 +596,7 @@ __global__ void __launch_bounds__(kWarpThreads)
     unsigned long long tot = 0;
 #pragma unroll
     for (int w = 0; w < 8; ++w) { tot += hist[w * 256 + b]; hist[w * 256 + b] = 0; }
-    if (tot) atomicAdd(out + size_t(sp.out_base + s) * 256 + b, tot);
+    if (tot) atomicAdd(out + size_t(sp.out_base + seg_row(sp, s)) * 256 + b, tot);
     __syncthreads();
   });
 }
@@ -622,7 +645,7 @@ __global__ void __launch_bounds__(kSubThreads)
       for (uint32_t j = 0; j < cnt; ++j) tot += slots[w * S + off + j];
     __syncthreads();
     for (int i = threadIdx.x; i < 8 * S; i += blockDim.x) slots[i] = 0;
-    if (tot) atomicAdd(out + size_t(sp.out_base + s) * 256 + b, tot);
+    if (tot) atomicAdd(out + size_t(sp.out_base + seg_row(sp, s)) * 256 + b, tot);
     __syncthreads();
   });
 }
@@ -1070,10 +1093,14 @@ int validate(const int64_t* off, const int64_t* cnt, int64_t S, int64_t cap) {
   return HS_OK;
 }
 
-int make_pattern(const int64_t* off, const int64_t* cnt, int64_t S, int64_t cap, PatternParams& pp) {
+// entries: the sub-bin kernels' packed (offset | count << 16) table is needed; it
+// limits total_slots to 16 bits. The lane kernels use only the hot bin, so any legal
+// pattern (total_slots up to 256 * cap, pattern.py:70-76) is accepted there.
+int make_pattern(const int64_t* off, const int64_t* cnt, int64_t S, int64_t cap, PatternParams& pp,
+                 bool entries = true) {
   int st = validate(off, cnt, S, cap);
   if (st != HS_OK) return st;
-  if (S > 65535) return HS_ERR_UNSUPPORTED;
+  if (entries && S > 65535) return HS_ERR_UNSUPPORTED;
   int64_t best = -1;
   int nbest = 0;
   pp.hot_bin = 0;
@@ -1164,6 +1191,9 @@ void split_grid(SegParams& sp, int grid, uint32_t split_cost = 0) {
   sp.q = units / g;
   sp.r = units % g;
   sp.units = units;
+  // plain split: CTA b has work iff it owns a unit (the last unit may be partial)
+  sp.merge_ctas = uint32_t(std::max<uint64_t>(1, std::min(g, units)) - 1);
+  if (sp.merge) split_cost = 0;  // no flush at segment boundaries: nothing to weigh
   sp.split_cost = sp.nseg > 1 && grid <= kMaxSplitGrid ? split_cost : 0;
   sp.lead_empty = 0;
   for (int s = 1; s < sp.nseg && sp.vstart[s] == 0; ++s) ++sp.lead_empty;
@@ -1220,7 +1250,7 @@ uint64_t lane_grid_for(uint64_t v, bool latency = false) {
 // one launch over the <= kMaxSeg (pieces of) segments prepared in sp
 int launch_batch(const uint8_t* d_data, SegParams& sp, int kind, int impl, const PatternParams* pp,
                  unsigned long long* d_out, cudaStream_t st, const DevInfo& di, const Tickets& tk,
-                 int reserve_slots = 0, bool latency = false) {
+                 int reserve_slots, bool latency, bool wait_first) {
   const uint64_t v = sp.vstart[sp.nseg];
   if (v == 0) return HS_OK;
   cudaError_t e = cudaSuccess;
@@ -1235,7 +1265,7 @@ int launch_batch(const uint8_t* d_data, SegParams& sp, int kind, int impl, const
     // weighted split only for full-grid launches with at least two CTAs per segment:
     // with several boundaries per CTA, or one CTA per SM, it measured slower
     // (256 x 1 MiB: 49.6 -> 55.7 us)
-    const bool weighted = want == ~0ull && 2 * sp.nseg <= grid;
+    const bool weighted = want == ~0ull && 2 * sp.nseg <= grid && !sp.merge;
     split_grid(sp, grid, weighted ? kLaneSplitCost : 0);
     const int hb = pp ? pp->hot_bin : 0;
     // ADAPTIVE runs the register path for the pattern's hot bin only when the pattern
@@ -1254,10 +1284,11 @@ int launch_batch(const uint8_t* d_data, SegParams& sp, int kind, int impl, const
     cfg.numAttrs = 1;
     if (hot) {
       cfg.blockDim = dim3(kLaneHotThreads);
-      e = cudaLaunchKernelEx(&cfg, k_lane<2, true, kLaneHotThreads, kLaneMinBlocks>, d_data, sp, hb, d_out, tk);
+      e = cudaLaunchKernelEx(&cfg, k_lane<2, true, kLaneHotThreads, kLaneMinBlocks>, d_data, sp, hb, d_out, tk,
+                             int(wait_first));
     } else {
       cfg.blockDim = dim3(kLaneThreads);
-      e = cudaLaunchKernelEx(&cfg, k_lane<2, false>, d_data, sp, hb, d_out, tk);
+      e = cudaLaunchKernelEx(&cfg, k_lane<2, false>, d_data, sp, hb, d_out, tk, int(wait_first));
     }
     if (e != cudaSuccess) return fold(e);
   } else if (impl == HS_IMPL_WARP) {
@@ -1296,7 +1327,8 @@ constexpr uint64_t kLaunchBytes = 1ull << 30;  // a word multiple, so every cut 
 
 int launch_segments(const uint8_t* d_data, const uint64_t* h_begin, const uint64_t* h_end, int s0, int ns,
                     int kind, int impl, const PatternParams* pp, unsigned long long* d_out, cudaStream_t st,
-                    const DevInfo& di, const Tickets& tk, int reserve_slots = 0, bool latency = false) {
+                    const DevInfo& di, const Tickets& tk, int reserve_slots, bool latency, bool& wait_first,
+                    bool merge = false, bool final_group = true) {
   uint64_t vs[kMaxSeg + 1];
   vs[0] = 0;
   for (int i = 0; i < ns; ++i) vs[i + 1] = vs[i] + (h_end[s0 + i] - h_begin[s0 + i]);
@@ -1309,6 +1341,8 @@ int launch_segments(const uint8_t* d_data, const uint64_t* h_begin, const uint64
     sp.nseg = 0;
     for (auto& w : sp.open_mask) w = 0;
     sp.acc_base = -1;
+    sp.merge = merge;
+    sp.merge_final = merge && final_group && last;
     for (int i = 0; i < ns; ++i) {
       // a non-empty segment joins every launch it intersects; an empty one the launch
       // holding its position (the last launch for positions at the very end)
@@ -1324,8 +1358,10 @@ int launch_segments(const uint8_t* d_data, const uint64_t* h_begin, const uint64
       if (vs[i + 1] > v1) sp.open_mask[k >> 5] |= 1u << (k & 31);
     }
     sp.out_base = s0 + sp.acc_base;
-    int rc = launch_batch(d_data, sp, kind, impl, pp, d_out, st, di, tk, reserve_slots, latency);
+    if (merge) sp.out_base = sp.acc_base = 0;  // one row for the whole call
+    int rc = launch_batch(d_data, sp, kind, impl, pp, d_out, st, di, tk, reserve_slots, latency, wait_first);
     if (rc != HS_OK) return rc;
+    wait_first = false;  // the rest of the call chains behind our own launches
   }
   return HS_OK;
 }
@@ -1390,7 +1426,9 @@ int histogram_batched(const uint8_t* d_data, const uint64_t* h_begin, const uint
                       uint64_t* d_out, void* d_ws, size_t ws_bytes, void* stream, bool latency) {
   if (nseg < 0 || (nseg > 0 && (!h_begin || !h_end || !d_out))) return HS_ERR_INVALID_ARG;
   const bool spread = (kind & HS_KIND_FLAG_SPREAD) != 0;
-  kind &= ~HS_KIND_FLAG_SPREAD;
+  bool wait_first = (kind & HS_KIND_FLAG_CHAINED) == 0;
+  const bool merge = (kind & HS_KIND_FLAG_MERGE) != 0;
+  kind &= ~(HS_KIND_FLAG_SPREAD | HS_KIND_FLAG_CHAINED | HS_KIND_FLAG_MERGE);
   if (kind != HS_KIND_NAIVE && kind != HS_KIND_ADAPTIVE) return HS_ERR_INVALID_ARG;
   if (impl < HS_IMPL_AUTO || impl > HS_IMPL_SUBBIN) return HS_ERR_INVALID_ARG;
   PatternParams pp;
@@ -1398,7 +1436,7 @@ int histogram_batched(const uint8_t* d_data, const uint64_t* h_begin, const uint
   if (kind == HS_KIND_ADAPTIVE && !have_pattern) return HS_ERR_INVALID_ARG;
   if (impl == HS_IMPL_SUBBIN && !have_pattern) return HS_ERR_INVALID_ARG;
   if (have_pattern) {
-    int rc = make_pattern(h_offset, h_count, total_slots, cap, pp);
+    int rc = make_pattern(h_offset, h_count, total_slots, cap, pp, impl == HS_IMPL_SUBBIN);
     if (rc != HS_OK) return rc;
     if (spread) pp.hot_unique = 0;  // caller's hint: no dominant value in the prior
   }
@@ -1424,22 +1462,31 @@ int histogram_batched(const uint8_t* d_data, const uint64_t* h_begin, const uint
     tk.ticket = reinterpret_cast<unsigned int*>(d_ws);
     tk.acc = reinterpret_cast<unsigned long long*>(reinterpret_cast<uint8_t*>(d_ws) + kTicketBytes);
     group = int(std::min<size_t>(kMaxSeg, (ws_bytes - kTicketBytes) / (256 * sizeof(uint64_t))));
+    if (merge) group = kMaxSeg;  // one accumulator row whatever the segment count
   } else {
-    cudaError_t e = cudaMemsetAsync(d_out, 0, size_t(nseg) * 256 * sizeof(uint64_t), st);
+    cudaError_t e = cudaMemsetAsync(d_out, 0, size_t(merge ? 1 : nseg) * 256 * sizeof(uint64_t), st);
     if (e != cudaSuccess) return fold(e);
   }
-  if (total == 0) return HS_OK;
+  if (total == 0) {
+    if (merge && tk.ticket != nullptr) return fold(cudaMemsetAsync(d_out, 0, 256 * sizeof(uint64_t), st));
+    return HS_OK;
+  }
+  // merged calls: the last group holding bytes finalizes the row
+  int last_busy = 0;
+  for (int s = 0; s < nseg; ++s) if (h_end[s] > h_begin[s]) last_busy = s;
   for (int s0 = 0; s0 < nseg; s0 += group) {
     const int ns = std::min(group, nseg - s0);
     bool empty = true;
     for (int i = 0; i < ns; ++i) empty = empty && h_end[s0 + i] == h_begin[s0 + i];
+    if (empty && merge) continue;
     if (empty && tk.ticket != nullptr) {
       cudaError_t e = cudaMemsetAsync(d_out + size_t(s0) * 256, 0, size_t(ns) * 256 * sizeof(uint64_t), st);
       if (e != cudaSuccess) return fold(e);
       continue;
     }
     rc = launch_segments(d_data, h_begin, h_end, s0, ns, kind, impl, have_pattern ? &pp : nullptr,
-                         reinterpret_cast<unsigned long long*>(d_out), st, di, tk, 0, latency);
+                         reinterpret_cast<unsigned long long*>(d_out), st, di, tk, 0, latency, wait_first, merge,
+                         last_busy < s0 + ns);
     if (rc != HS_OK) return rc;
   }
   return HS_OK;
@@ -1497,7 +1544,8 @@ int hs_histogram_sync(const uint8_t* d_data, const uint64_t* h_begin, const uint
   int rc = histogram_batched(d_data, h_begin, h_end, nseg, kind, impl, h_offset, h_count, total_slots, cap, d_out,
                              d_ws, ws_bytes, stream, true);
   if (rc != HS_OK || nseg == 0) return rc;
-  cudaError_t e = cudaMemcpyAsync(h_out, d_out, size_t(nseg) * 256 * sizeof(uint64_t), cudaMemcpyDeviceToHost, st);
+  const size_t rows = (kind & HS_KIND_FLAG_MERGE) ? 1 : size_t(nseg);
+  cudaError_t e = cudaMemcpyAsync(h_out, d_out, rows * 256 * sizeof(uint64_t), cudaMemcpyDeviceToHost, st);
   if (e != cudaSuccess) return fold(e);
   return fold(cudaStreamSynchronize(st));
 }
@@ -1532,7 +1580,8 @@ int hs_histogram_host(const uint8_t* const* h_chunks, const uint64_t* h_sizes, i
   int rc = histogram_batched(d_stage, begin.data(), end.data(), nseg, kind, impl, h_offset, h_count, total_slots,
                              cap, d_out, d_ws, ws_bytes, stream, true);
   if (rc != HS_OK) return rc;
-  cudaError_t e = cudaMemcpyAsync(h_out, d_out, size_t(nseg) * 256 * sizeof(uint64_t), cudaMemcpyDeviceToHost, st);
+  const size_t rows = (kind & HS_KIND_FLAG_MERGE) ? 1 : size_t(nseg);
+  cudaError_t e = cudaMemcpyAsync(h_out, d_out, rows * 256 * sizeof(uint64_t), cudaMemcpyDeviceToHost, st);
   if (e != cudaSuccess) return fold(e);
   return fold(cudaStreamSynchronize(st));
 }
@@ -1545,9 +1594,15 @@ int hs_histogram(const uint8_t* d_data, uint64_t n_bytes, int kind, int impl, co
                               d_ws, ws_bytes, stream);
 }
 
+size_t hs_group_slots_ws_bytes(int group_size, int group_count, int64_t total_slots, int mode) {
+  if (group_size < 1 || group_count < 1 || total_slots < 1 || mode < 0 || mode > 2) return 0;
+  // mode 2 only: exact totals in u64 before the 16-bit wrap
+  return mode == 2 ? size_t(group_count) * size_t(total_slots) * sizeof(uint64_t) : 0;
+}
+
 int hs_group_slots(const uint8_t* d_data, uint64_t n_bytes, int group_size, int group_count,
                    const int64_t* h_offset, const int64_t* h_count, int64_t total_slots, int64_t cap,
-                   int mode, void* d_out, void* stream) {
+                   int mode, void* d_out, void* d_ws, size_t ws_bytes, void* stream) {
   if (group_size < 1 || group_count < 1 || mode < 0 || mode > 2 || !d_out) return HS_ERR_INVALID_ARG;
   if (n_bytes & 3) return HS_ERR_ALIGNMENT;
   if (n_bytes && !d_data) return HS_ERR_INVALID_ARG;
@@ -1561,9 +1616,9 @@ int hs_group_slots(const uint8_t* d_data, uint64_t n_bytes, int group_size, int 
   unsigned long long* acc = nullptr;
   cudaError_t e;
   if (mode == 2) {
-    // exact 64-bit totals in a scratch buffer, then wrapped to 16 bits
-    e = cudaMallocAsync(reinterpret_cast<void**>(&acc), n_out * 8, st);
-    if (e != cudaSuccess) return fold(e);
+    // exact 64-bit totals in the caller's workspace, then wrapped to 16 bits
+    if (!d_ws || ws_bytes < n_out * 8) return HS_ERR_WORKSPACE;
+    acc = reinterpret_cast<unsigned long long*>(d_ws);
   } else {
     acc = reinterpret_cast<unsigned long long*>(d_out);
   }
@@ -1580,7 +1635,6 @@ int hs_group_slots(const uint8_t* d_data, uint64_t n_bytes, int group_size, int 
     const int grid = int(std::min<uint64_t>((n_out + 255) / 256, 4096));
     k_wrap16<<<grid, 256, 0, st>>>(acc, reinterpret_cast<uint16_t*>(d_out), n_out);
     if ((e = cudaGetLastError()) != cudaSuccess) return fold(e);
-    if ((e = cudaFreeAsync(acc, st)) != cudaSuccess) return fold(e);
   }
   return HS_OK;
 }
@@ -1661,8 +1715,12 @@ int hs_stream_step(const uint8_t* d_data, const uint64_t* h_begin, const uint64_
     // The histogram does not wait for the previous fold's decision: both kinds count
     // exactly the same, so the lane kernel runs for either and streams while the fold
     // (one CTA) finishes on the side; the decided kind is what the log records.
+    // chained: the step's stream predecessor is the previous step's fold or
+    // hs_stream_reset (the batch must be complete before that was issued; see hist256.h)
+    bool wait_first = false;
     rc = launch_segments(d_data, h_begin, h_end, 0, nseg, HS_KIND_NAIVE, HS_IMPL_LANE, nullptr,
-                         reinterpret_cast<unsigned long long*>(d_out), st, di, tk, /*reserve_slots=*/1);
+                         reinterpret_cast<unsigned long long*>(d_out), st, di, tk, /*reserve_slots=*/1, false,
+                         wait_first);
     if (rc != HS_OK) return rc;
   }
   // pattern and kernel refresh for iteration+1 when (iteration+1) % every == 0 (stream.py:407-414)

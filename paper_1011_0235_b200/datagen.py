@@ -111,7 +111,13 @@ def generate_device(spec: SourceSpec, data, first_pixel: int = 0, stream=None):
     spec.validate()
     if spec.kind not in (UNIFORM, SEQUENTIAL, CONSTANT, NORMAL):
         raise SpecInvalid(f"{spec.kind} has a data-dependent draw count: generate it on the host")
-    s = (stream or torch.cuda.current_stream()).cuda_stream
+    if (not isinstance(data, torch.Tensor) or not data.is_cuda or data.dtype != torch.uint8
+            or not data.is_contiguous()):
+        raise TypeError("generate_device needs a contiguous uint8 CUDA tensor")
+    st = stream or torch.cuda.current_stream(data.device)
+    if st.device != data.device:
+        raise ValueError(f"tensor on {data.device} but stream on {st.device}")
+    s = st.cuda_stream
     N.check(N.lib().hs_generate_device(_GEN_ID[spec.kind], spec.seed & _MASK64, int(spec.value),
                                        float(spec.mean), float(spec.sigma), int(first_pixel),
                                        data.data_ptr(), data.numel(), s), "hs_generate_device")

@@ -125,7 +125,8 @@ class Staging:
         self._dev = None
         self._out_host = None
         self._out_dev = None
-        self._ws = None
+        self._ws: dict[int, object] = {}  # stream handle -> workspace (insertion = LRU order)
+        self._cap: dict[int, object] = {}  # the same during a CUDA-graph capture
         self._one = None  # _OneCall: prepared arguments of the one-chunk blocking calls
 
     def device_bytes(self, n: int):
@@ -136,15 +137,44 @@ class Staging:
         # 256-B aligned start (the allocator returns 512-B aligned blocks)
         return self._dev
 
-    def workspace(self):
-        """Device workspace of hs_histogram_batched (per-segment tickets + partials),
-        zeroed once; every launch leaves its tickets at zero again. Launches that
-        share it must be stream-ordered (one staging per stream user)."""
-        if self._ws is None:
-            t = torch()
+    _MAX_WS = 32
+
+    def workspace(self, stream=None):
+        """Device workspace of hs_histogram_batched (per-segment tickets + partials) for
+        launches on ``stream`` (a torch stream, a raw handle, or None for the current
+        stream), zeroed once; every launch leaves it zero again. Launches that share a
+        workspace must be stream-ordered, so there is one per CUDA stream: two calls on
+        unsynchronized streams never share accumulator rows. Each is allocated and
+        zeroed on its own stream, so the caching allocator only ever hands its memory
+        back to work ordered after it."""
+        t = torch()
+        if stream is None:
+            h = _raw_stream(self.device.index)
+        else:
+            h = int(stream) if isinstance(stream, int) else int(stream.cuda_stream)
+        if t.cuda.is_current_stream_capturing():
+            # Inside a CUDA-graph capture nothing executes: a workspace created here is
+            # zeroed by a memset node of the graph (and lives in the graph's private
+            # pool), so it serves only launches of this capture and never leaks into
+            # eager use. One per stream per capture; dropped once capturing ends.
+            ws = self._cap.get(h)
+            if ws is None:
+                n = int(N.lib().hs_workspace_bytes(256))
+                with t.cuda.stream(t.cuda.ExternalStream(h, device=self.device)):
+                    ws = t.zeros(max(n, 256), dtype=t.uint8, device=self.device)
+                self._cap[h] = ws
+            return ws
+        if self._cap:
+            self._cap.clear()
+        ws = self._ws.get(h)
+        if ws is None:
             n = int(N.lib().hs_workspace_bytes(256))  # launches of up to 256 segments
-            self._ws = t.zeros(max(n, 256), dtype=t.uint8, device=self.device)
-        return self._ws
+            if len(self._ws) >= self._MAX_WS:  # bounded: drop the least recently created
+                self._ws.pop(next(iter(self._ws)))
+            with t.cuda.stream(t.cuda.ExternalStream(h, device=self.device)):
+                ws = t.zeros(max(n, 256), dtype=t.uint8, device=self.device)
+            self._ws[h] = ws
+        return ws
 
     def device_out(self, nseg: int):
         """Device int64 [nseg, 256] counts buffer for the synchronous host path."""
@@ -160,23 +190,26 @@ class Staging:
             self._out_host = t.empty(max(need, 64 * BINS), dtype=t.int64, pin_memory=True)
         return self._out_host[:need]
 
-    def one_call(self, n_bytes: int = 0) -> "_OneCall":
-        """Arguments of one-chunk blocking calls (the per-image path), built once: the
-        device, host and workspace buffers are only ever replaced by larger ones, so
-        the cached pointers stay valid until a buffer grows."""
+    def one_call(self, stream: int, n_bytes: int = 0) -> "_OneCall":
+        """Arguments of one-chunk blocking calls (the per-image path) on raw stream
+        ``stream``, built once: the device, host and workspace buffers are only ever
+        replaced by larger ones, so the cached pointers stay valid until a buffer grows
+        or the stream changes."""
         one = self._one
-        if (one is None or one.out_dev is not self._out_dev or one.h_out is not self._out_host
+        if (one is None or one.stream != stream or one.out_dev is not self._out_dev or one.h_out is not self._out_host
                 or one.dev is not self._dev or (n_bytes and (self._dev is None or self._dev.numel() < n_bytes))):
             if n_bytes:
                 self.device_bytes(n_bytes)
-            one = self._one = _OneCall(self, self.device_out(1), self.host_out(1), self.workspace(), self._dev)
+            one = self._one = _OneCall(self, self.device_out(1), self.host_out(1), self.workspace(stream), self._dev,
+                                       stream)
         return one
 
 
 class _OneCall:
     """ctypes arguments of hs_histogram_sync / hs_histogram_host for one chunk."""
 
-    def __init__(self, staging: Staging, out_dev, h_out, ws, dev):
+    def __init__(self, staging: Staging, out_dev, h_out, ws, dev, stream: int):
+        self.stream = stream
         self.out_dev = staging._out_dev  # the owning tensors (identity = validity)
         self.h_out = staging._out_host
         self.dev = staging._dev
@@ -225,6 +258,10 @@ def stage(chunks: Sequence, staging: Staging | None, stream=None) -> StagedBatch
     pinned) into ``staging``'s buffer at word-aligned offsets on ``stream``; device
     chunks are referenced in place. Records ``ready`` after the copies."""
     t = require_cuda()
+    dev_index = staging.device.index if staging is not None else t.cuda.current_device()
+    for c in chunks:
+        if type(c) is DeviceChunk and c._dev != dev_index:
+            raise ValueError(f"DeviceChunk on cuda:{c._dev} staged for cuda:{dev_index}")
     if chunks and all(type(c) is DeviceChunk for c in chunks):
         # fast path (device-resident batches, e.g. the device stream engine): addresses
         # and sizes are cached on the chunks, so staging 64 chunks is a few microseconds
@@ -319,7 +356,7 @@ def launch(staged: StagedBatch, kind: int, pattern=None, stream=None, impl: int 
     workspace. Returns the device int64 tensor [nseg, 256] (reinterpret as uint64)."""
     t = require_cuda()
     stream = stream or t.cuda.current_stream()
-    ws = (staging or default_staging()).workspace()
+    ws = (staging or default_staging()).workspace(stream)
     if staged.ready is not None:
         stream.wait_event(staged.ready)
     nseg = staged.nseg
@@ -403,7 +440,9 @@ def _one_histogram(chunk, kind, pattern, impl, st: "Staging") -> np.ndarray:
     stream = _raw_stream(st.device.index)
     kind = int(_with_hints(kind, pattern))
     if type(chunk) is DeviceChunk:
-        one = st.one_call()
+        if chunk._dev != st.device.index:
+            raise ValueError(f"DeviceChunk on cuda:{chunk._dev} used on cuda:{st.device.index}")
+        one = st.one_call(stream)
         off_p, cnt_p, S, cap = one.pattern_ptrs(pattern)
         n = chunk._n
         one.end[0] = n
@@ -413,7 +452,7 @@ def _one_histogram(chunk, kind, pattern, impl, st: "Staging") -> np.ndarray:
         N.check(status, "hs_histogram_sync")
     else:
         n = chunk.byte_size
-        one = st.one_call(max(n, 16))
+        one = st.one_call(stream, max(n, 16))
         off_p, cnt_p, S, cap = one.pattern_ptrs(pattern)
         one.end[0] = n
         one.ptrs[0] = chunk.words.ctypes.data if n else None
@@ -436,7 +475,7 @@ def _host_histograms(chunks, kind, pattern, impl, st: "Staging", stream) -> np.n
     dev = st.device_bytes(max(need, 16))
     out_dev = st.device_out(n)
     h_out = st.host_out(n)  # pinned: the D2H stays a DMA
-    ws = st.workspace()
+    ws = st.workspace(stream)
     off_p, cnt_p, S, cap, keep = _pattern_args(pattern)
     status = N.lib().hs_histogram_host(ptrs, N.u64p(sizes), n, int(_with_hints(kind, pattern)), int(impl),
                                        off_p, cnt_p, S, cap, dev.data_ptr(), dev.numel(), out_dev.data_ptr(),
@@ -453,7 +492,7 @@ def _sync_histograms(staged: StagedBatch, kind, pattern, impl, st: "Staging", st
     n = staged.nseg
     out_dev = st.device_out(n)
     h_out = st.host_out(n)
-    ws = st.workspace()
+    ws = st.workspace(stream)
     off_p, cnt_p, S, cap, keep = _pattern_args(pattern)
     begin = np.ascontiguousarray(staged.begin, dtype=np.uint64)
     end = np.ascontiguousarray(staged.end, dtype=np.uint64)
@@ -487,8 +526,11 @@ def group_slots(chunk, pattern, group_size: int, group_count: int, mode: int) ->
     out = t.empty(shape, dtype=dtype, device=t.cuda.current_device())
     off_p, cnt_p, S, cap, keep = _pattern_args(pattern)
     base = staged.base + int(staged.begin[0]) if staged.nbytes else 0
+    ws_n = int(N.lib().hs_group_slots_ws_bytes(int(group_size), int(group_count), S, int(mode)))
+    ws = t.empty(max(ws_n, 8), dtype=t.uint8, device=t.cuda.current_device())
     status = N.lib().hs_group_slots(base or None, staged.nbytes, int(group_size), int(group_count),
-                                    off_p, cnt_p, S, cap, int(mode), out.data_ptr(), stream.cuda_stream)
+                                    off_p, cnt_p, S, cap, int(mode), out.data_ptr(), ws.data_ptr(), ws_n,
+                                    stream.cuda_stream)
     N.check(status, "hs_group_slots")
     host = out.cpu().numpy()
     return host.view(np.uint16) if mode == 2 else host.view(np.uint64)

@@ -14,6 +14,9 @@ if str(ROOT) not in sys.path:
 
 GOLDEN_DIR = ROOT / "tests" / "golden"
 
+# the vendored reference suites run only through their harnesses (subprocess + shim)
+collect_ignore = ["refsuites", "refshim"]
+
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and libhist256.so")

@@ -1,8 +1,9 @@
-"""The N>1 path on CPU: world_size-2 gloo processes shard a stream by contiguous
-byte range (distributed.shard_range, the group_ranges rule) and join 256-count
-partials with one all_reduce; the result equals the whole-stream histogram.
-Per-shard counts come from the oracle here (no GPU); the device path swaps in
-libhist256 and NCCL with the same host logic (bench.py)."""
+"""The N>1 path on CPU: world_size-2/3 gloo processes go through the product API
+(distributed.init_process_group + ShardedHistogram): each rank takes its contiguous
+byte range (the group_ranges rule), counts it, and one all_reduce of the 256-count
+partials joins them; the result equals the whole-stream histogram. The per-shard count
+comes from the oracle through ShardedHistogram's test-only count_fn hook (no GPU); on
+the B200 the same object runs one merged libhist256 call per rank and NCCL."""
 import os
 import socket
 
@@ -22,9 +23,12 @@ def _free_port() -> int:
 
 
 def _worker(rank, world, port, n_bytes, kind, q):
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank), HS_DIST_VERBOSE="0")
+    from paper_1011_0235_b200.distributed import ShardedHistogram, init_process_group
+
+    r, w, _ = init_process_group("gloo")
+    assert (r, w) == (rank, world)
     try:
         import sys
         from pathlib import Path
@@ -33,11 +37,19 @@ def _worker(rank, world, port, n_bytes, kind, q):
         from oracle import oracle as O
 
         px = O.generate(kind, n_bytes, seed=99, mean=128.0, sigma=32.0, value=3)
-        lo, hi = shard_range(n_bytes, rank, world)
-        counts = torch.from_numpy(O.histogram(px[lo:hi]).view(np.int64).copy())
-        allreduce_counts(counts)
-        if rank == 0:
-            q.put((as_uint64(counts), O.histogram(px)))
+        seen = []
+
+        def count_fn(shard):  # test-only hook: the oracle instead of the device kernel
+            seen.append(shard.size)
+            return torch.from_numpy(O.histogram(shard).view(np.int64).copy())
+
+        sh = ShardedHistogram(count_fn=count_fn)
+        lo, hi = sh.shard(n_bytes)
+        assert (lo, hi) == shard_range(n_bytes, rank, world)
+        sh(px[lo:hi])
+        hist = sh.result()
+        assert seen == [hi - lo]
+        q.put((rank, hist.counts, O.histogram(px)))
     finally:
         dist.destroy_process_group()
 
@@ -50,11 +62,20 @@ def test_sharded_allreduce_equals_whole(world, n_bytes, kind):
     procs = [ctx.Process(target=_worker, args=(r, world, port, n_bytes, kind, q)) for r in range(world)]
     for p in procs:
         p.start()
-    got, want = q.get(timeout=120)
+    res = [q.get(timeout=120) for _ in range(world)]
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
-    assert np.array_equal(got, want)
+    assert sorted(r for r, _, _ in res) == list(range(world))
+    for _, got, want in res:  # every rank holds the whole stream's histogram
+        assert np.array_equal(got, want)
+
+
+def test_allreduce_counts_gloo_direct():
+    """allreduce_counts is a no-op outside a process group."""
+    c = torch.arange(256, dtype=torch.int64)
+    assert allreduce_counts(c) is c and int(c.sum()) == 255 * 128
+    assert np.array_equal(as_uint64(c), np.arange(256, dtype=np.uint64))
 
 
 def test_shard_ranges_cover_stream():
