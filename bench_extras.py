@@ -77,7 +77,8 @@ def c1_image(hs, N, torch, dev):
     s = torch.cuda.current_stream()
 
     def batched():
-        N.check(L.hs_histogram_batched(imgs.data_ptr(), N.u64p(b0), N.u64p(b1), C1_IMAGES, N.HS_KIND_NAIVE, 0, None,
+        N.check(L.hs_histogram_batched(imgs.data_ptr(), N.u64p(b0), N.u64p(b1), C1_IMAGES,
+                                       N.HS_KIND_NAIVE | N.HS_KIND_FLAG_CHAINED, 0, None,
                                        None, 0, 0, out.data_ptr(), ws.data_ptr(), ws.numel(), s.cuda_stream), "batched")
 
     for _ in range(3):
@@ -105,7 +106,8 @@ def c1_image(hs, N, torch, dev):
     with torch.cuda.graph(g):
         gs = torch.cuda.current_stream()
         for _ in range(100):
-            N.check(L.hs_histogram_batched(imgs.data_ptr(), N.u64p(one0), N.u64p(one1), 1, N.HS_KIND_NAIVE, 0, None,
+            N.check(L.hs_histogram_batched(imgs.data_ptr(), N.u64p(one0), N.u64p(one1), 1,
+                                           N.HS_KIND_NAIVE | N.HS_KIND_FLAG_CHAINED, 0, None,
                                            None, 0, 0, out1.data_ptr(), ws.data_ptr(), ws.numel(), gs.cuda_stream),
                     "capture")
     g.replay()
@@ -203,6 +205,7 @@ def c2_normal_streams(hs, N, torch, dev, steps: int = 20):
     pending = {}
     kinds = set()
     b_p, e_p = N.u64p(begin), N.u64p(end)
+    torch.cuda.synchronize()  # inputs generated and workspaces zeroed (current stream) before the side streams
 
     def launch(j, k):
         if j in pending:
@@ -212,7 +215,7 @@ def c2_normal_streams(hs, N, torch, dev, steps: int = 20):
             patterns[j] = hs.compute_binning_pattern(hs.Histogram256(prior))
         p = patterns[j]
         kind = D._with_hints(N.HS_KIND_ADAPTIVE, p) | N.HS_KIND_FLAG_CHAINED
-        kinds.add("k_lane<HOT> (register path)" if not kind & N.HS_KIND_FLAG_SPREAD else "k_lane plain core (spread hint)")
+        kinds.add(D.kernel_form(kind, p))
         N.check(L.hs_histogram_batched(streams[j].data_ptr(), b_p, e_p, 64, kind, N.HS_IMPL_AUTO, N.i64p(p.offset),
                                        N.i64p(p.count), 960, 8, outs[j][k].data_ptr(), wss[j].data_ptr(),
                                        wss[j].numel(), side[j].cuda_stream), "c2")

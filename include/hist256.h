@@ -57,11 +57,12 @@ extern "C" {
 #define HS_KIND_FLAG_SPREAD 0x100
 /* OR-ed into kind: the caller guarantees that the kernel preceding this call on the
  * stream is a libhist256 launch (for instance the previous call over the same resident
- * input) and that the input was complete before that launch was issued. The call's
+ * input) and that the input was complete before that launch started (written before
+ * a stream synchronisation, or before an earlier call that has completed). The call's
  * first launch may then start streaming before its predecessor finishes (programmatic
- * dependent launch). Without it the first launch waits for its predecessor before its
- * first load, so input written by ANY preceding kernel -- including producers that
- * trigger their dependents early -- is read only once complete. */
+ * dependent launch). Without it the first launch waits for its predecessor -- complete
+ * and its writes visible -- before its first load, so input written by ANY preceding
+ * kernel, including producers that trigger their dependents early, is read complete. */
 #define HS_KIND_FLAG_CHAINED 0x200
 /* OR-ed into kind: merge every segment into ONE histogram, d_out = uint64[256] = the
  * sum over all nseg segments (merge_all of the per-slice histograms, core.py:152-156),

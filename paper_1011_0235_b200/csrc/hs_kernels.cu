@@ -506,8 +506,9 @@ __device__ __forceinline__ uint32_t lane_piece(const uint8_t* __restrict__ data,
 
 // HOT (ADAPTIVE): register path for the hot bin `hot_bin`.
 // wait_first: the first launch of a public call, whose stream predecessor may be the
-// kernel that wrote the input: wait for it before the first load and only then let
-// the next launch start (so a chained launch after us never overtakes that producer).
+// kernel that wrote the input: wait for it (griddepcontrol.wait: complete and flushed)
+// before the first load. The next launch is still allowed to become resident early;
+// if it too waits first, it waits for us, hence transitively for our producer.
 // Chained launches (later launches of the same call, hs_stream_step, or a caller's
 // HS_KIND_FLAG_CHAINED) stream before their predecessor -- a libhist256 kernel, which
 // never writes the input -- has finished, and wait only before their first write.
@@ -523,8 +524,8 @@ __global__ void __launch_bounds__(TH, MB)
   __shared__ int pc_seg[kMaxSeg];
   __shared__ int pc_n;
   HS_STAMP(0);
-  if (wait_first) pdl_wait();
   pdl_launch_dependents();  // the next launch's CTAs may take SMs as ours retire
+  if (wait_first) pdl_wait();
   if (threadIdx.x == 0) {
     int n = 0;
     for_each_piece<~0ull>(sp, [&](int s, uint64_t p0, uint64_t p1) {

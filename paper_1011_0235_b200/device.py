@@ -349,6 +349,22 @@ def _with_hints(kind: int, pattern) -> int:
     return kind
 
 
+def kernel_form(kind: int, pattern=None, impl: int = N.HS_IMPL_AUTO) -> str:
+    """The device kernel a hs_histogram_batched call with these arguments runs (the
+    library's own rule, hs_kernels.cu launch_batch): for labels that must name what ran."""
+    if impl == N.HS_IMPL_WARP:
+        return "k_warp"
+    if impl == N.HS_IMPL_SUBBIN:
+        return "k_subbin"
+    base = kind & ~(N.HS_KIND_FLAG_SPREAD | N.HS_KIND_FLAG_CHAINED | N.HS_KIND_FLAG_MERGE)
+    if base == N.HS_KIND_ADAPTIVE and pattern is not None and not kind & N.HS_KIND_FLAG_SPREAD:
+        c = np.asarray(pattern.count)
+        top = int(c.max())
+        if top > 1 and int((c == top).sum()) == 1:
+            return f"k_lane<HOT> (register path for bin {int(np.argmax(c))})"
+    return "k_lane (lane-banked core)"
+
+
 def launch(staged: StagedBatch, kind: int, pattern=None, stream=None, impl: int = N.HS_IMPL_AUTO, out=None,
            staging: Staging | None = None):
     """hs_histogram_batched on ``stream`` (waits for the staging copies first): one

@@ -198,6 +198,20 @@ for i, (segs, iters, pixels, batch, every, window) in enumerate(scen):
         "kernel_log": [k.value for k in log], "chunks_seen": acc.chunks_seen,
     })
 
+# 8. genealogy stage checksums (run_ablation, kernels.py:421-496): seeded chunk, pattern
+# from the data, several group counts (SUBHIST and FULL checksums depend on them)
+meta["ablation"] = []
+for i, (kind, px, seed, gc) in enumerate([("uniform", 1 << 14, 11, 2), ("normal", 1 << 14, 3, 3),
+                                          ("mixture", 4096 + 12, 5, 1), ("uniform", 1 << 16, 12, 4),
+                                          ("sequential", 1 << 12, 0, 5)]):
+    spec = SourceSpec(kind, px, seed, mean=128.0, sigma=20.0, value=200, degeneracy=0.6)
+    chunk = generate(spec)
+    pattern = ref.compute_binning_pattern(ref.reference_histogram(chunk))
+    cfg = ref.WorkerGroupConfig(8, gc)
+    sums = {st.value: int(ref.run_ablation(chunk, st, pattern, cfg).checksum) for st in ref.ABLATION_STAGES}
+    arrays[f"ablation_{i}_pixels"] = unpack_chunk(chunk)
+    meta["ablation"].append({"spec": spec_dict(spec), "group_size": 8, "group_count": gc, "checksums": sums})
+
 np.savez_compressed(OUT / "reference_vectors.npz", **arrays)
 (OUT / "reference_vectors.json").write_text(json.dumps(meta, indent=1))
 print(f"wrote {len(arrays)} arrays, {len(meta['streams'])} streams", file=sys.stderr)
