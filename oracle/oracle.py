@@ -89,6 +89,27 @@ def histogram_mt(pixels: np.ndarray, threads: int | None = None, piece: int = 64
     return out
 
 
+def ablation_checksums(pixels: np.ndarray, offset, count, group_count: int) -> dict:
+    """The genealogy stages' checksums (run_ablation, kernels.py:421-496, workers
+    :212-264): copy_only / copy_init XOR every 32-bit word (copy_init adds slot 0 of a
+    zeroed array); pattern_load XORs offset[b] + count[b] over every pixel;
+    subhist_noreduce XORs each group's slot sum (its pixel count); full XORs counts[0]
+    once per group. XOR is order independent, so lanes and groups drop out except where
+    the per-group sums enter."""
+    p = np.ascontiguousarray(pixels, dtype=np.uint8)
+    words = p.view("<u4")
+    x = int(np.bitwise_xor.reduce(words.astype(np.uint64))) if words.size else 0
+    table = (np.asarray(offset, np.int64) + np.asarray(count, np.int64)).astype(np.uint64)
+    pl = int(np.bitwise_xor.reduce(table[p])) if p.size else 0
+    sub = 0
+    full = 0
+    c0 = int(histogram(p)[0])
+    for start, stop in group_ranges(words.size, group_count):
+        sub ^= 4 * (stop - start)
+        full ^= c0
+    return {"copy_only": x, "copy_init": x, "pattern_load": pl, "subhist_noreduce": sub, "full": full}
+
+
 def group_ranges(word_count: int, group_count: int) -> list[tuple[int, int]]:
     """kernels.py:311-316 (the C restatement, returned as Python tuples)."""
     st = np.zeros(group_count, np.int64)

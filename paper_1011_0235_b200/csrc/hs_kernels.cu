@@ -9,7 +9,7 @@
 //                                            the segment's last CTA (integer adds commute: exact)
 //   batch_histograms  stream.py:260-316   -> one launch per <= kMaxSeg segments and <= 1 GiB
 //   _adaptive_worker_traced / _u16        -> k_group_slots (reference group/lane mapping)
-//   _stage_*_worker   kernels.py:212-264  -> k_ablation
+//   _stage_*_worker   kernels.py:212-264  -> k_genealogy (production skeleton)
 //   _fill_*           datagen.py:98-133   -> k_gen_*
 //
 // Design notes (numbers in DESIGN.md §4, tools/microbench/hist_variants.cu):
@@ -199,16 +199,7 @@ __device__ unsigned long long hs_trace_buf[1024][16];
 __device__ __forceinline__ uint32_t byte_of(uint32_t w, int k) { return __byte_perm(w, 0u, 0x4440u | k); }
 
 // ------------------------------------------------------------------ segment walk
-// Block b owns the word-aligned virtual range [vb, ve) of the concatenated segments.
-__device__ __forceinline__ void block_range(uint64_t total, uint64_t& vb, uint64_t& ve) {
-  // whole kSplitWords units per CTA, as the SegParams split below (line-aligned loads)
-  const uint64_t units = ((total >> 2) + kSplitWords - 1) / kSplitWords, g = gridDim.x, b = blockIdx.x;
-  const uint64_t q = units / g, r = units % g;
-  const uint64_t u0 = q * b + min(b, r), u1 = u0 + q + (b < r ? 1 : 0);
-  vb = min(total & ~uint64_t(3), 4 * kSplitWords * u0);
-  ve = min(total & ~uint64_t(3), 4 * kSplitWords * u1);
-}
-
+// Block b owns the word-aligned virtual range [vb, ve) of the concatenated segments:
 // The same split with the host's q, r (SegParams launches)
 __device__ __forceinline__ void block_range(const SegParams& sp, uint64_t& vb, uint64_t& ve) {
   const uint64_t b = blockIdx.x, total = sp.vstart[sp.nseg];
@@ -335,6 +326,12 @@ __device__ __forceinline__ EachVec<U, VecFn> each_vec(VecFn& f) { return EachVec
 #ifndef HS_LANE_THREADS
 #define HS_LANE_THREADS 1024
 #define HS_LANE_BLOCKS 2
+#endif
+// How a call's first launch (wait_first) orders itself behind its stream predecessor:
+// 0 = PDL launch, trigger dependents at entry, then griddepcontrol.wait before loading;
+// 1 = PDL launch, wait first, then trigger; 2 = no PDL attribute (plain stream order).
+#ifndef HS_FIRST_LAUNCH
+#define HS_FIRST_LAUNCH 1
 #endif
 constexpr int kLaneThreads = HS_LANE_THREADS;
 constexpr int kLaneBlocks = HS_LANE_BLOCKS;
@@ -524,8 +521,13 @@ __global__ void __launch_bounds__(TH, MB)
   __shared__ int pc_seg[kMaxSeg];
   __shared__ int pc_n;
   HS_STAMP(0);
+#if HS_FIRST_LAUNCH == 1
+  if (wait_first) pdl_wait();
+  pdl_launch_dependents();  // the next launch's CTAs may take SMs as ours retire
+#else
   pdl_launch_dependents();  // the next launch's CTAs may take SMs as ours retire
   if (wait_first) pdl_wait();
+#endif
   if (threadIdx.x == 0) {
     int n = 0;
     for_each_piece<~0ull>(sp, [&](int s, uint64_t p0, uint64_t p1) {
@@ -681,71 +683,120 @@ __global__ void k_wrap16(const unsigned long long* __restrict__ in, uint16_t* __
 }
 
 // ================================================================== ablation (genealogy)
-// Cumulative stages on the sub-bin skeleton (kernels.py:212-264, :421-496).
-__global__ void __launch_bounds__(kSubThreads)
-    k_ablation(const uint8_t* __restrict__ data, uint64_t n_bytes, int stage,
-               const __grid_constant__ PatternParams pp, unsigned long long* __restrict__ sink,
-               unsigned long long* __restrict__ out) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  uint32_t* lut = reinterpret_cast<uint32_t*>(smem);
-  uint32_t* slots = lut + 256 * 32;
-  const int S = pp.total_slots;
-  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (stage >= HS_STAGE_PATTERN_LOAD) {
-    for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) {
-      const uint32_t b = i >> 5, l = i & 31, e = pp.entry[b];
-      lut[i] = ((e & 0xffff) + l % (e >> 16)) * 4;
-    }
+// The paper's Table 1 (run_ablation, kernels.py:212-264, :421-496): cumulative stages on
+// the PRODUCTION skeleton -- k_lane's 1024-thread CTAs, two per SM, 16-B streaming loads
+// in 4 KiB-aligned CTA ranges -- with shared memory only from the stage that needs it:
+//   COPY_ONLY         read every word, XOR checksum                   (no shared memory)
+//   COPY_INIT         + zero the 32 KB lane-banked counter array       (32 KB)
+//   PATTERN_LOAD      + per pixel, read the pattern's entry for its bin from a lane-banked
+//                       table (offset[b] + count[b], the reference's per-pixel load) (64 KB)
+//   SUBHIST_NOREDUCE  + per pixel, increment the (bin, lane) sub-counter -- on the B200
+//                       a bin's sub-bins are its 32 lane columns
+//   FULL              + reduce the 32 columns per bin and merge into d_out (u64 RED)
+// Sinks: COPY_* the XOR of every 32-bit word, PATTERN_LOAD the XOR over pixels of
+// offset[b] + count[b] -- both the reference's values; SUBHIST/FULL the number of
+// increments (the host turns it into the reference's per-group form).
+template <int U, int TH, class WordFn, class VecFn>
+__device__ __forceinline__ void gen_piece(const uint8_t* __restrict__ data, uint64_t p0, uint64_t p1,
+                                          WordFn&& word, VecFn&& vec) {
+  constexpr uint32_t T = TH;
+  const uint32_t tid = threadIdx.x;
+  const uint64_t base = reinterpret_cast<uintptr_t>(data);
+  const uint64_t a0 = min(p1, ((base + p0 + 15) & ~uint64_t(15)) - base);
+  const uint64_t a1 = max(a0, ((base + p1) & ~uint64_t(15)) - base);
+  if (p0 + 4ull * tid < a0) word(*reinterpret_cast<const uint32_t*>(data + p0 + 4ull * tid));
+  if (a1 + 4ull * tid < p1) word(*reinterpret_cast<const uint32_t*>(data + a1 + 4ull * tid));
+  const uint32_t nv = uint32_t((a1 - a0) >> 4);
+  uint32_t nfull = nv / (U * T);
+  {
+    const uint4* __restrict__ r = reinterpret_cast<const uint4*>(data + a0);
+    for (uint32_t i = nfull * U * T + tid; i < nv; i += T) vec(ldg_stream(r + i));
   }
-  if (stage >= HS_STAGE_COPY_INIT)
-    for (int i = threadIdx.x; i < 8 * S; i += blockDim.x) slots[i] = 0;
-  __syncthreads();
-  const uint32_t lb = (uint32_t)__cvta_generic_to_shared(lut) + lane * 4;
-  const uint32_t wb = (uint32_t)__cvta_generic_to_shared(slots) + warp * S * 4;
-  unsigned long long x = 0;
-  auto word = [&](uint32_t w) {
-    if (stage <= HS_STAGE_COPY_INIT) { x ^= w; return; }
-    if (stage == HS_STAGE_PATTERN_LOAD) {
+  const uint4* __restrict__ q = reinterpret_cast<const uint4*>(data + a0) + tid;
+  uint4 A[U], B[U];
+  if (nfull > 0) {
 #pragma unroll
-      for (int k = 0; k < 4; ++k) x ^= sh_ld(lb + (byte_of(w, k) << 7));
-      return;
+    for (int u = 0; u < U; ++u) A[u] = ldg_stream(q + u * T);
+  }
+  while (nfull >= 2) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) B[u] = ldg_stream(q + (U + u) * T);
+#pragma unroll
+    for (int u = 0; u < U; ++u) vec(A[u]);
+    if (nfull > 2) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) A[u] = ldg_stream(q + (2 * U + u) * T);
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) sh_inc(wb + sh_ld(lb + (byte_of(w, k) << 7)));
+    for (int u = 0; u < U; ++u) vec(B[u]);
+    q += 2 * U * T;
+    nfull -= 2;
+  }
+  if (nfull == 1) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) vec(A[u]);
+  }
+}
+
+template <int STAGE>
+__global__ void __launch_bounds__(kLaneThreads, kLaneBlocks)
+    k_genealogy(const uint8_t* __restrict__ data, uint64_t n_bytes, uint64_t q, uint64_t r,
+                const __grid_constant__ PatternParams pp, unsigned long long* __restrict__ sink,
+                unsigned long long* __restrict__ out) {
+  extern __shared__ __align__(16) uint32_t gsm[];
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t cbase = (uint32_t)__cvta_generic_to_shared(gsm);  // counters [256][32]
+  const uint32_t tbase = cbase + kLaneArrayBytes;                    // table    [256][32]
+  if (STAGE >= HS_STAGE_COPY_INIT)
+    for (uint32_t i = threadIdx.x; i < kLaneArrayBytes / 16; i += blockDim.x) sh_st4(cbase + i * 16, make_uint4(0, 0, 0, 0));
+  if (STAGE >= HS_STAGE_PATTERN_LOAD)
+    for (uint32_t i = threadIdx.x; i < 256 * 32; i += blockDim.x) {
+      const uint32_t e = pp.entry[i >> 5];
+      sh_st(tbase + i * 4, (e & 0xffffu) + (e >> 16));
+    }
+  if (STAGE >= HS_STAGE_COPY_INIT) __syncthreads();
+  const uint32_t col = lane * 4;
+  uint32_t x = 0;
+  auto word = [&](uint32_t w) {
+    if (STAGE <= HS_STAGE_COPY_INIT) {
+      x ^= w;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t off = (byte_of(w, k) << 7) + col;
+        x ^= sh_ld(tbase + off);
+        if (STAGE >= HS_STAGE_SUBHIST_NOREDUCE) sh_inc(cbase + off);
+      }
+    }
   };
   auto vec = [&](const uint4& v) { word(v.x); word(v.y); word(v.z); word(v.w); };
-  uint64_t vb, ve;
-  block_range(n_bytes, vb, ve);
-  if (vb < ve) stream_range<8, 2>(data, vb, ve, word, vec, each_vec<8>(vec));
+  // the CTA's whole 4 KiB units (q, r from the host: no 64-bit division on the device)
+  const uint64_t b = blockIdx.x;
+  const uint64_t u0 = q * b + min(b, r), u1 = u0 + q + (b < r ? 1 : 0);
+  const uint64_t vb = min(n_bytes, 4 * kSplitWords * u0), ve = min(n_bytes, 4 * kSplitWords * u1);
+  // the copy stages finish a vector in one LOP3 per word, so ptxas would hoist the loads
+  // of both buffers and spill at U = 2 under the 32-register budget: one vector per buffer
+  constexpr int U = STAGE <= HS_STAGE_COPY_INIT ? 1 : 2;
+  if (vb < ve) gen_piece<U, kLaneThreads>(data, vb, ve, word, vec);
+  if (STAGE <= HS_STAGE_PATTERN_LOAD) {
+    // XOR is order independent: the reference's checksum whatever the schedule
+    for (int o = 16; o; o >>= 1) x ^= __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0 && x) atomicXor(sink, (unsigned long long)x);
+    return;
+  }
+  asm volatile("" ::"r"(x));  // the table loads stay part of the measured work
   compiler_fence();
   __syncthreads();
-  if (stage <= HS_STAGE_PATTERN_LOAD) {
-    // xor is order independent: deterministic checksum
-    for (int o = 16; o; o >>= 1) x ^= __shfl_xor_sync(0xffffffffu, x, o);
-    if (lane == 0 && x) atomicXor(sink, x);
+  if (STAGE == HS_STAGE_SUBHIST_NOREDUCE) {
+    // sink += every sub-counter of the CTA (the reference: sum of every slot, :462-463)
+    unsigned long long t = 0;
+    for (uint32_t i = threadIdx.x; i < 256 * 32; i += blockDim.x) t += sh_ld(cbase + i * 4);
+    for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane == 0 && t) atomicAdd(sink, t);
     return;
   }
-  const int b = threadIdx.x;
-  const uint32_t e = pp.entry[b], off = e & 0xffff, cnt = e >> 16;
-  unsigned long long tot = 0;
-  if (stage == HS_STAGE_SUBHIST_NOREDUCE) {
-    // sink = sum of every slot (kernels.py:462-463): reduced in the CTA first, so the
-    // stage pays one global atomic per CTA, not one per thread on a single address
-    for (int i = threadIdx.x; i < 8 * S; i += blockDim.x) tot += slots[i];
-    for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-    __shared__ unsigned long long warp_tot[kSubThreads / 32];
-    if (lane == 0) warp_tot[warp] = tot;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      unsigned long long t = 0;
-      for (int w = 0; w < kSubThreads / 32; ++w) t += warp_tot[w];
-      if (t) atomicAdd(sink, t);
-    }
-    return;
-  }
-  for (int w = 0; w < 8; ++w)
-    for (uint32_t j = 0; j < cnt; ++j) tot += slots[w * S + off + j];
-  if (tot) atomicAdd(out + b, tot);
+  lane_flush(cbase, out, false);  // FULL: reduce_subbins + merge (u64 RED per bin)
+  if (threadIdx.x == 0 && vb < ve) atomicAdd(sink, (unsigned long long)(ve - vb));
 }
 
 // ================================================================== device stream engine
@@ -761,7 +812,9 @@ struct DevStreamHeader {
   uint32_t pad0[3];
   unsigned long long chunks_seen;
   unsigned long long t_reset_ns;  // %globaltimer when hs_stream_reset ran
-  unsigned long long pad1[2];
+  double decided_degeneracy;      // window degeneracy at the last decision (the host's
+                                  // lagged choice of the register path reads it)
+  unsigned long long pad1;
 };
 static_assert(sizeof(DevStreamHeader) == 64, "header size");
 
@@ -988,6 +1041,7 @@ __global__ void __maxnreg__(128)
     if (decide) {  // decision for the next iteration (lag 1)
       hd->kind = frac >= threshold ? HS_KIND_ADAPTIVE : HS_KIND_NAIVE;
       hd->hot = r.am;
+      hd->decided_degeneracy = frac;
     }
     hd->head = head;
     hd->count = count;
@@ -1008,6 +1062,167 @@ __global__ void __maxnreg__(128)
     if (ns_log) ns_log[iteration] = globaltimer_ns();
   }
   HS_FSTAMP(5);
+}
+
+
+// ------------------------------------------------------------------ block engine
+// Several iterations per launch chain (hs_stream_block): the histograms of all their
+// chunks in ONE histogram call, then the per-iteration fold of every iteration at once.
+// The fold is exact integer algebra over the sequence E = (ring, oldest first) ++ (the
+// block's chunk histograms h_0..h_{m-1}): with prefix sums PE[k] = sum of E[0..k),
+//   window after iteration i = PE[c0 + c_i] - PE[max(0, c0 + c_i - W)]
+//   acc after iteration i    = acc_prev + PE[c0 + c_i] - PE[c0]
+// (c0 = ring entries before the block, c_i = chunks up to and including iteration i),
+// the same integers the reference's incremental push/evict gives (stream.py:141-178).
+// Every entry is a device-made histogram (non-negative), so the window never goes
+// negative (the NegativeCount guard of the per-step fold has nothing to catch here).
+//   k_block_scan    local inclusive prefix of E in tiles of kScanTile rows + tile totals
+//   k_block_fold    one CTA per iteration: window, acc, degeneracy, divergence -> logs
+//   k_block_commit  one CTA: kind log and lag-1 decisions in order, acc/window/ring/head
+constexpr int kScanTile = 16;
+constexpr int kBlockMaxIter = 256;
+constexpr int kBlockMaxChunks = kMaxSeg;
+
+struct BlockMap {                 // per-block layout, host-computed
+  int n_iter, m, c0_unused;
+  int first_iteration;
+  int end_chunk[kBlockMaxIter];   // c_i: chunks of iterations 0..i of the block
+};
+
+__device__ __forceinline__ const unsigned long long* e_row(const unsigned long long* ring, int W, uint32_t head,
+                                                           int c0, const unsigned long long* hist, int k) {
+  if (k < c0) {
+    int slot = int(head) + k;
+    if (slot >= W) slot -= W;
+    return ring + size_t(slot) * 256;
+  }
+  return hist + size_t(k - c0) * 256;
+}
+
+// grid = ceil((c0 + m) / kScanTile) CTAs x 256 threads (bin b = thread)
+__global__ void __launch_bounds__(256) k_block_scan(const unsigned long long* __restrict__ hist, int m,
+                                                    const uint8_t* __restrict__ state, int W,
+                                                    unsigned long long* __restrict__ local,
+                                                    unsigned long long* __restrict__ tile_tot) {
+  pdl_launch_dependents();
+  pdl_wait();  // the block's histogram launch is complete
+  const DevStreamHeader* hd = reinterpret_cast<const DevStreamHeader*>(state);
+  const unsigned long long* ring = reinterpret_cast<const unsigned long long*>(state + sizeof(DevStreamHeader)) + 512;
+  const int c0 = int(hd->count), R = c0 + m, b = threadIdx.x;
+  const uint32_t head = hd->head;
+  const int k0 = blockIdx.x * kScanTile;
+  unsigned long long v[kScanTile];
+#pragma unroll
+  for (int j = 0; j < kScanTile; ++j) v[j] = (k0 + j < R) ? __ldcg(e_row(ring, W, head, c0, hist, k0 + j) + b) : 0ull;
+  unsigned long long s = 0;
+#pragma unroll
+  for (int j = 0; j < kScanTile; ++j) {
+    s += v[j];
+    if (k0 + j < R) local[size_t(k0 + j) * 256 + b] = s;  // inclusive: E[k0..k0+j]
+  }
+  tile_tot[size_t(blockIdx.x) * 256 + b] = s;
+}
+
+// PE[k] (sum of E[0..k)) for bin b from the tile scan
+__device__ __forceinline__ unsigned long long pe_at(const unsigned long long* local, const unsigned long long* tile_tot,
+                                                    int k, int b) {
+  if (k <= 0) return 0ull;
+  const int last = k - 1, t = last / kScanTile;
+  unsigned long long s = __ldcg(local + size_t(last) * 256 + b);
+  for (int j = 0; j < t; ++j) s += __ldcg(tile_tot + size_t(j) * 256 + b);
+  return s;
+}
+
+// one CTA (256 threads) per iteration of the block
+__global__ void __launch_bounds__(256) k_block_fold(const __grid_constant__ BlockMap bm, uint8_t* __restrict__ state,
+                                                    int W, const unsigned long long* __restrict__ local,
+                                                    const unsigned long long* __restrict__ tile_tot,
+                                                    double* __restrict__ deg_log, double* __restrict__ div_log,
+                                                    uint32_t* __restrict__ argmax_out) {
+  __shared__ double d[256];
+  __shared__ double acc16[16];
+  pdl_launch_dependents();
+  pdl_wait();
+  DevStreamHeader* hd = reinterpret_cast<DevStreamHeader*>(state);
+  const unsigned long long* acc_prev = reinterpret_cast<const unsigned long long*>(state + sizeof(DevStreamHeader));
+  const int i = blockIdx.x, b = threadIdx.x;
+  const int c0 = int(hd->count), ci = c0 + bm.end_chunk[i];
+  const int lo = max(0, ci - W);
+  const unsigned long long pci = pe_at(local, tile_tot, ci, b);
+  const unsigned long long w = pci - pe_at(local, tile_tot, lo, b);
+  const unsigned long long a = acc_prev[b] + (pci - pe_at(local, tile_tot, c0, b));
+  const FoldRed r = fold_reduce(a, w, b);
+  const double frac = r.tb ? __ddiv_rn((double)r.mx, (double)r.tb) : 0.0;
+  const double pa = r.ta ? __ddiv_rn((double)a, (double)r.ta) : 0.0;
+  const double pb = r.tb ? __ddiv_rn((double)w, (double)r.tb) : 0.0;
+  d[b] = fabs(__dadd_rn(pa, -pb));
+  __syncthreads();
+  const double tv = np_pairwise_sum256(d, acc16);
+  if (b == 0) {
+    const int it = bm.first_iteration + i;
+    deg_log[it] = frac;
+    div_log[it] = __dmul_rn(0.5, tv);
+    argmax_out[i] = r.am;
+    if (r.ta == 0 || r.tb == 0) atomicOr(&hd->error, 2u);
+  }
+}
+
+// one CTA: the decisions in iteration order and the state after the block
+__global__ void __launch_bounds__(256) k_block_commit(const __grid_constant__ BlockMap bm,
+                                                      const unsigned long long* __restrict__ hist,
+                                                      uint8_t* __restrict__ state, int W, double threshold,
+                                                      int recompute_every, const unsigned long long* __restrict__ local,
+                                                      const unsigned long long* __restrict__ tile_tot,
+                                                      const double* __restrict__ deg_log,
+                                                      const uint32_t* __restrict__ argmax_in,
+                                                      int32_t* __restrict__ kind_log,
+                                                      unsigned long long* __restrict__ ns_log) {
+  pdl_wait();  // every iteration's fold is done (and with it the histogram and the scan)
+  DevStreamHeader* hd = reinterpret_cast<DevStreamHeader*>(state);
+  unsigned long long* acc = reinterpret_cast<unsigned long long*>(state + sizeof(DevStreamHeader));
+  unsigned long long* win = acc + 256;
+  unsigned long long* ring = win + 256;
+  const int b = threadIdx.x, m = bm.m;
+  const int c0 = int(hd->count);
+  const uint32_t head = hd->head;
+  const int R = c0 + m;
+  // acc and window after the block's last iteration
+  const unsigned long long pR = pe_at(local, tile_tot, R, b);
+  acc[b] += pR - pe_at(local, tile_tot, c0, b);
+  win[b] = pR - pe_at(local, tile_tot, max(0, R - W), b);
+  // ring: push k of the block sits in slot (head + c0 + k) mod W; only the last W survive
+  {
+    const int j0 = max(0, m - W);
+    int slot = int((uint32_t(head) + uint32_t(c0) + uint32_t(j0)) % uint32_t(W));
+    for (int j = j0; j < m; ++j) {
+      ring[size_t(slot) * 256 + b] = __ldcg(hist + size_t(j) * 256 + b);
+      slot = slot + 1 == W ? 0 : slot + 1;
+    }
+  }
+  __syncthreads();
+  if (b == 0) {
+    uint32_t kind = hd->kind, hot = hd->hot;
+    double dd = hd->decided_degeneracy;
+    const unsigned long long now = globaltimer_ns();
+    for (int i = 0; i < bm.n_iter; ++i) {
+      const int it = bm.first_iteration + i;
+      kind_log[it] = int32_t(kind);
+      if (ns_log) ns_log[it] = now;
+      if (((it + 1) % recompute_every) == 0) {  // decision for the next iteration (lag 1)
+        const double frac = deg_log[it];
+        kind = frac >= threshold ? HS_KIND_ADAPTIVE : HS_KIND_NAIVE;
+        hot = argmax_in[i];
+        dd = frac;
+      }
+    }
+    hd->kind = kind;
+    hd->hot = hot;
+    hd->decided_degeneracy = dd;
+    const int ev = max(0, R - W);
+    hd->head = uint32_t((uint32_t(head) + uint32_t(ev)) % uint32_t(W));
+    hd->count = uint32_t(min(W, R));
+    hd->chunks_seen += uint64_t(m);
+  }
 }
 
 // ================================================================== generators
@@ -1282,7 +1497,7 @@ int launch_batch(const uint8_t* d_data, SegParams& sp, int kind, int impl, const
     // PDL overlaps a launch's ramp with the previous launch's tail (in the device
     // stream engine: with the previous iteration's one-CTA fold)
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = (HS_FIRST_LAUNCH == 2 && wait_first) ? 0 : 1;  // mode 2: plain stream order
     if (hot) {
       cfg.blockDim = dim3(kLaneHotThreads);
       e = cudaLaunchKernelEx(&cfg, k_lane<2, true, kLaneHotThreads, kLaneMinBlocks>, d_data, sp, hb, d_out, tk,
@@ -1657,15 +1872,35 @@ int hs_ablation_stage(const uint8_t* d_data, uint64_t n_bytes, int stage, const 
   if (e != cudaSuccess) return fold(e);
   if (d_out256 && (e = cudaMemsetAsync(d_out256, 0, 2048, st)) != cudaSuccess) return fold(e);
   if (n_bytes == 0) return HS_OK;
-  const size_t smem = (256 * 32 + 8 * size_t(total_slots)) * 4;
-  if (smem > (size_t)di.smem_optin) return HS_ERR_UNSUPPORTED;
-  if ((rc = set_smem(k_ablation, smem)) != HS_OK) return rc;
-  const int per_sm = std::max(1, int(di.smem_optin / (smem + 1024)));
-  const uint64_t want = (n_bytes + (64ull << 10) - 1) / (64ull << 10);
-  const int grid = int(std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(di.sms) * per_sm)));
-  k_ablation<<<grid, kSubThreads, smem, st>>>(d_data, n_bytes, stage, pp,
-                                               reinterpret_cast<unsigned long long*>(d_sink),
-                                               reinterpret_cast<unsigned long long*>(d_out256));
+  // shared memory only from the stage that uses it (none for the copy baseline)
+  const size_t smem = stage == HS_STAGE_COPY_ONLY ? 0 : stage == HS_STAGE_COPY_INIT ? kLaneArrayBytes
+                                                                                     : 2 * size_t(kLaneArrayBytes);
+  const int grid = int(std::max<uint64_t>(1, std::min<uint64_t>(lane_grid_for(n_bytes), uint64_t(di.sms) * kLaneBlocks)));
+  const uint64_t units = ((n_bytes >> 2) + kSplitWords - 1) / kSplitWords;
+  const uint64_t q = units / uint64_t(grid), r = units % uint64_t(grid);
+  auto* sk = reinterpret_cast<unsigned long long*>(d_sink);
+  auto* ot = reinterpret_cast<unsigned long long*>(d_out256);
+  static std::atomic<uint64_t> set2{0}, set3{0}, set4{0};
+  switch (stage) {
+    case HS_STAGE_COPY_ONLY:
+      k_genealogy<HS_STAGE_COPY_ONLY><<<grid, kLaneThreads, 0, st>>>(d_data, n_bytes, q, r, pp, sk, ot);
+      break;
+    case HS_STAGE_COPY_INIT:
+      k_genealogy<HS_STAGE_COPY_INIT><<<grid, kLaneThreads, smem, st>>>(d_data, n_bytes, q, r, pp, sk, ot);
+      break;
+    case HS_STAGE_PATTERN_LOAD:
+      if ((rc = set_smem_once(k_genealogy<HS_STAGE_PATTERN_LOAD>, smem, set2)) != HS_OK) return rc;
+      k_genealogy<HS_STAGE_PATTERN_LOAD><<<grid, kLaneThreads, smem, st>>>(d_data, n_bytes, q, r, pp, sk, ot);
+      break;
+    case HS_STAGE_SUBHIST_NOREDUCE:
+      if ((rc = set_smem_once(k_genealogy<HS_STAGE_SUBHIST_NOREDUCE>, smem, set3)) != HS_OK) return rc;
+      k_genealogy<HS_STAGE_SUBHIST_NOREDUCE><<<grid, kLaneThreads, smem, st>>>(d_data, n_bytes, q, r, pp, sk, ot);
+      break;
+    default:
+      if ((rc = set_smem_once(k_genealogy<HS_STAGE_FULL>, smem, set4)) != HS_OK) return rc;
+      k_genealogy<HS_STAGE_FULL><<<grid, kLaneThreads, smem, st>>>(d_data, n_bytes, q, r, pp, sk, ot);
+      break;
+  }
   return fold(cudaGetLastError());
 }
 

@@ -177,14 +177,32 @@ def compute_histogram(chunk, kind: KernelKind, pattern: BinningPattern | None,
 def run_ablation(chunk, variant: KernelKind, pattern: BinningPattern, cfg: WorkerGroupConfig) -> AblationTiming:
     """One genealogy stage on the device (kernels.py:421-496, Table 1).
 
-    Stages are cumulative on the sub-bin kernel skeleton: read (+xor checksum), + zero
-    the slot arrays, + per-pixel pattern lookup, + sub-bin atomics, + fused reduce and
-    merge. Duration is CUDA-event device time of the stage's launch."""
+    Stages are cumulative on the production (k_lane) skeleton: read (+XOR checksum),
+    + zero the lane-banked counters, + per-pixel pattern load, + per-pixel sub-counter
+    increment, + reduce and merge (hs_kernels.cu k_genealogy). Duration is the mean
+    CUDA-event device time of back-to-back launches of the stage (device.ablation_stage).
+
+    Checksums are the reference's values: COPY_* the XOR of every word, PATTERN_LOAD the
+    XOR over pixels of offset[b] + count[b] (both computed on the device);
+    SUBHIST_NOREDUCE the XOR over the ``cfg`` groups of each group's slot sum (its pixel
+    count) once the device's increment total equals the pixel count; FULL counts[0]
+    XOR-ed once per group (kernels.py:462-473)."""
     if variant not in ABLATION_STAGES:
         raise ValueError(f"{variant} is not an ablation stage")
     validate_pattern(pattern)
     _check_chunk(chunk)
-    seconds, checksum, hist = D.ablation_stage(chunk, _STAGE_ID[variant], pattern)
+    seconds, sink, hist = D.ablation_stage(chunk, _STAGE_ID[variant], pattern)
+    ranges = group_ranges(chunk.byte_size // 4, cfg.group_count)
+    checksum = sink
+    if variant is KernelKind.SUBHIST_NOREDUCE:
+        if sink == chunk.byte_size:  # every pixel incremented one sub-counter
+            checksum = 0
+            for start, stop in ranges:
+                checksum ^= 4 * (stop - start)
+    elif variant is KernelKind.FULL:
+        checksum = 0
+        for _ in ranges:
+            checksum ^= int(hist[0])
     throughput = chunk.byte_size / seconds if seconds > 0 else float("inf")
     return AblationTiming(variant, seconds, throughput, checksum, Histogram256(hist) if hist is not None else None)
 

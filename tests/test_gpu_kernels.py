@@ -223,18 +223,27 @@ def test_reduce_subbins(cuda):
         hs.reduce_subbins(np.zeros(959, np.uint64), p)
 
 
-def test_ablation_stages(cuda):
+def test_ablation_stages(cuda, golden, oracle):
+    """Genealogy stages on the device give the reference's own checksums (reference-
+    generated run_ablation outputs, tests/golden) and, at 4 Mi pixels, the oracle's."""
+    for i, case in enumerate(golden.meta["ablation"]):
+        px = golden[f"ablation_{i}_pixels"]
+        chunk = hs.PackedChunk(oracle.pack(px))
+        pattern = hs.compute_binning_pattern(hs.reference_histogram(chunk))
+        cfg = hs.WorkerGroupConfig(case["group_size"], case["group_count"])
+        for stage in hs.ABLATION_STAGES:
+            got = hs.run_ablation(chunk, stage, pattern, cfg)
+            assert got.checksum == case["checksums"][stage.value], (i, stage)
     chunk = hs.generate(hs.SourceSpec("uniform", 1 << 22, seed=13))
     pattern = hs.compute_binning_pattern(hs.reference_histogram(chunk))
     cfg = hs.WorkerGroupConfig(32, 2)
     full = hs.run_ablation(chunk, hs.KernelKind.FULL, pattern, cfg)
     assert full.histogram == hs.reference_histogram(chunk) and full.throughput_bps > 0
+    want = oracle.ablation_checksums(chunk.pixels(), pattern.offset, pattern.count, 2)
     for stage in hs.ABLATION_STAGES:
         a = hs.run_ablation(chunk, stage, pattern, cfg)
         b = hs.run_ablation(chunk, stage, pattern, cfg)
-        assert a.checksum == b.checksum
-    sub = hs.run_ablation(chunk, hs.KernelKind.SUBHIST_NOREDUCE, pattern, cfg)
-    assert sub.checksum == chunk.pixel_count  # sum of every slot
+        assert a.checksum == b.checksum == want[stage.value], stage
     with pytest.raises(ValueError):
         hs.run_ablation(chunk, hs.KernelKind.NAIVE, pattern, cfg)
 

@@ -234,3 +234,13 @@ def test_stream_fold_matches_reference(golden):
         assert r["degeneracy_log"] == golden[f"stream_{i}_deg"].tolist()
         assert r["divergence_log"] == golden[f"stream_{i}_div"].tolist()
         assert r["chunks_seen"] == m["chunks_seen"]
+
+
+def test_ablation_checksums_match_reference(golden):
+    """The genealogy stages' checksums (run_ablation, kernels.py:421-496) on the
+    reference's own outputs: seeded chunks, data patterns, 1..5 groups."""
+    for i, case in enumerate(golden.meta["ablation"]):
+        px = golden[f"ablation_{i}_pixels"]
+        off, cnt = O.binning_pattern(O.histogram(px).tolist(), 960, 8)
+        got = O.ablation_checksums(px, off, cnt, case["group_count"])
+        assert got == case["checksums"], (i, got, case["checksums"])
