@@ -130,18 +130,27 @@ def c1_image(hs, N, torch, dev):
 
 
 def c3_switch(hs, torch, dev):
-    """BASELINE configs[2]: a stream that turns degenerate -- uniform, then a bimodal
-    peak (50/50 of bytes 40 and 200; not a reference generator: uniform bytes < 128 map
-    to 40, the rest to 200), then constant 127 -- as C2-sized iterations (64 x 16 MiB =
-    1 GiB each, two per segment), through the device-resident engine: the window,
-    accumulator and lag-1 NVHist/AHist switch live on the GPU (run_device_stream)."""
-    px, per_iter, iters_per_seg = CHUNK, 64, 2
-    segs = ("uniform", "bimodal", "constant")
-    total = len(segs) * iters_per_seg * per_iter
+    """BASELINE configs[2]: a stream that turns degenerate -- 1 GiB uniform, then 1 GiB of
+    a bimodal peak (50/50 of bytes 40 and 200; not a reference generator: uniform bytes
+    < 128 map to 40, the rest to 200), then 2 GiB constant 127 -- in 16 MiB chunks,
+    iterations of 16 chunks (256 MiB), through the device-resident engine
+    (run_device_stream: window, accumulator and the lag-1 NVHist/AHist switch on the
+    GPU, one block of iterations per histogram call). Once the device has decided
+    ADAPTIVE on the constant window, the engine runs the register path for bin 127.
+    Per-segment device rates from the commit kernels' device clock; the accumulator is
+    checked bin for bin (closed form for the bimodal/constant parts, oracle for the
+    uniform part)."""
+    from oracle import oracle as O
+
+    px, per_iter = CHUNK, 16
+    plan = (("uniform", 4), ("bimodal", 4), ("constant", 8))  # iterations per segment
+    iters = sum(n for _, n in plan)
+    total = iters * per_iter
     buf = torch.empty(total * px, dtype=torch.uint8, device=dev)
     k = 0
-    for kind in segs:
-        for _ in range(iters_per_seg * per_iter):
+    seg_of = []
+    for kind, n in plan:
+        for _ in range(n * per_iter):
             sl = buf[k * px:(k + 1) * px]
             if kind == "constant":
                 hs.generate_device(hs.SourceSpec("constant", px, k, value=127), sl)
@@ -150,29 +159,44 @@ def c3_switch(hs, torch, dev):
                 if kind == "bimodal":
                     sl.copy_((sl >= 128).to(torch.uint8) * 160 + 40)
             k += 1
-    iters = total // per_iter
-    cfg = hs.PipelineConfig(num_iterations=iters, chunk_pixels=px, batch_size=per_iter, window_size=1)
-
+        seg_of += [kind] * n
+    torch.cuda.synchronize()
+    cfg = hs.PipelineConfig(num_iterations=iters, chunk_pixels=px, batch_size=per_iter, window_size=per_iter)
     batches = [[hs.DeviceChunk(buf[(i * per_iter + j) * px:(i * per_iter + j + 1) * px]) for j in range(per_iter)]
                for i in range(iters)]  # views built once, outside the timed call
 
-    def src():
-        yield from batches
-
-    hs.run_device_stream(src(), cfg, hs.SwitchPolicy())
+    hs.run_device_stream(iter(batches), cfg, hs.SwitchPolicy())
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    acc, _, rep, log = hs.run_device_stream(src(), cfg, hs.SwitchPolicy())
+    acc, _, rep, log = hs.run_device_stream(iter(batches), cfg, hs.SwitchPolicy())
     wall = time.perf_counter() - t0
-    assert acc.running.total() == total * px
-    # device time from the folds' device-clock stamps; iteration 0 also holds the host's
-    # first staging after the reset, so the steady-state rate is taken over 1..n-1
-    dev_ns = sum(s.compute_ns for s in rep.stages[1:])
-    return {"bytes": total * px, "chunks": total, "iterations": iters,
-            "device_gbs": round((iters - 1) * per_iter * px / dev_ns, 1),
-            "device_gbs_method": "device clock between consecutive folds, iterations 1..n-1",
-            "wall_gbs": round(total * px / wall / 1e9, 1),
-            "kernel_log": [k.value for k in log], "degeneracy_log": [round(d, 4) for d in rep.degeneracy_log]}
+    uni = O.histogram_mt(buf[:4 * per_iter * px].cpu().numpy())
+    bim = buf[4 * per_iter * px:8 * per_iter * px]
+    n40 = int((bim == 40).sum().item())
+    want = uni.copy()
+    want[40] += n40
+    want[200] += 4 * per_iter * px - n40
+    want[127] += 8 * per_iter * px
+    assert np.array_equal(acc.running.counts, want), "C3 accumulator"
+    it_bytes = per_iter * px
+    rates = {}
+    for kind, _ in plan:  # iteration 0 also holds the host's first staging: excluded
+        idx = [i for i in range(1, iters) if seg_of[i] == kind]
+        ns = sum(rep.stages[i].compute_ns for i in idx)
+        rates[kind] = round(len(idx) * it_bytes / ns, 1) if ns else None
+    hot = [i for i, e in enumerate(rep.executed_log) if "HOT" in e]
+    hot_ns = sum(rep.stages[i].compute_ns for i in hot)
+    del buf
+    torch.cuda.empty_cache()
+    return {"bytes": total * px, "chunks": total, "iterations": iters, "iteration_bytes": it_bytes,
+            "device_gbs_by_segment": rates,
+            "device_gbs_register_path_iterations": round(len(hot) * it_bytes / hot_ns, 1) if hot_ns else None,
+            "device_gbs_method": "commit kernels' device clock (block time split over its iterations), iterations 1..n-1",
+            "wall_gbs": round(total * px / wall / 1e9, 1), "blocks": rep.block_sizes,
+            "host_issue_us_per_block": round(rep.host_issue_ns / 1e3 / len(rep.block_sizes), 1),
+            "kernel_log": [k.value for k in log], "executed_log": rep.executed_log,
+            "degeneracy_log": [round(d, 4) for d in rep.degeneracy_log],
+            "parity": "accumulator == oracle (uniform part) + closed forms (bimodal, constant), bin for bin"}
 
 
 def c2_normal_streams(hs, N, torch, dev, steps: int = 20):

@@ -220,6 +220,32 @@ int hs_stream_step(const uint8_t* d_data, const uint64_t* h_begin, const uint64_
                    uint64_t* d_out, double* d_deg_log, double* d_div_log, int32_t* d_kind_log,
                    uint64_t* d_ns_log, void* d_ws, size_t ws_bytes, void* stream);
 
+/* Several iterations per call: the block engine behind run_device_stream. The nseg
+ * (<= 256) chunk segments of n_iter (<= 256) consecutive iterations -- iteration i owns
+ * the next h_iter_chunks[i] segments -- are counted in ONE histogram call into
+ * d_out[nseg][256], then three small kernels fold every iteration exactly as n_iter
+ * successive hs_stream_step folds would (same state, same logs at
+ * [first_iteration, first_iteration + n_iter), bit for bit): window and accumulator per
+ * iteration from prefix sums over (ring ++ block chunks), degeneracy/decision/divergence
+ * per iteration in parallel, then the lag-1 decisions in order and the new state.
+ * hot_bin >= 0 runs the histogram's register path for that bin (the caller's lagged
+ * view of the ADAPTIVE decision, state header: kind at byte 0, hot bin at byte 4, the
+ * deciding degeneracy as a double at byte 48); -1 the plain core -- counts are
+ * identical. d_ns_log: every iteration of the block gets the commit's device clock.
+ * h_decision (may be NULL): page-locked host uint64[3] the commit kernel writes after
+ * the block -- [1] kind | hot << 32, [2] the deciding degeneracy (double bits), then
+ * [0] = first_iteration + n_iter (written last, after a system fence): the host reads
+ * the device's latest decision without an event or copy.
+ * Workspace: hs_stream_block_ws_bytes(window_size, nseg) bytes, 16-byte aligned, zeroed
+ * once by the caller (every call leaves its tickets zero again). Input contract as
+ * hs_stream_step (the histogram is chained behind the previous block's commit). */
+size_t hs_stream_block_ws_bytes(int window_size, int max_chunks);
+int hs_stream_block(const uint8_t* d_data, const uint64_t* h_begin, const uint64_t* h_end, int nseg,
+                    const int32_t* h_iter_chunks, int n_iter, void* d_state, int window_size, double threshold,
+                    int recompute_every, int first_iteration, int hot_bin, uint64_t* d_out, double* d_deg_log,
+                    double* d_div_log, int32_t* d_kind_log, uint64_t* d_ns_log, uint64_t* h_decision,
+                    void* d_ws, size_t ws_bytes, void* stream);
+
 /* ---- host-side control plane (native replacements of pattern.py / policy.py) */
 
 /* compute_binning_pattern (pattern.py:94-133) / uniform_pattern (pattern.py:85-91 when

@@ -77,6 +77,8 @@ EXPORTED = (
     "hs_stream_state_bytes",
     "hs_stream_reset",
     "hs_stream_step",
+    "hs_stream_block_ws_bytes",
+    "hs_stream_block",
 )
 
 _c = ctypes
@@ -130,6 +132,12 @@ _SIGNATURES = {
     ),
     "hs_stream_state_bytes": (_c.c_size_t, [_c.c_int]),
     "hs_stream_reset": (_c.c_int, [_P, _c.c_int, _P]),
+    "hs_stream_block_ws_bytes": (_c.c_size_t, [_c.c_int, _c.c_int]),
+    "hs_stream_block": (
+        _c.c_int,
+        [_P, _U64P, _U64P, _c.c_int, _c.POINTER(_c.c_int32), _c.c_int, _P, _c.c_int, _c.c_double, _c.c_int,
+         _c.c_int, _c.c_int, _P, _P, _P, _P, _P, _P, _P, _c.c_size_t, _P],
+    ),
     "hs_stream_step": (
         _c.c_int,
         [_P, _U64P, _U64P, _c.c_int, _P, _c.c_int, _c.c_double, _c.c_int, _c.c_int, _P, _P, _P, _P, _P, _P,

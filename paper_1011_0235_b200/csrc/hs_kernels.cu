@@ -1099,11 +1099,15 @@ __device__ __forceinline__ const unsigned long long* e_row(const unsigned long l
   return hist + size_t(k - c0) * 256;
 }
 
-// grid = ceil((c0 + m) / kScanTile) CTAs x 256 threads (bin b = thread)
+// grid = ceil((W + m) / kScanTile) CTAs x 256 threads (bin b = thread). Each CTA scans
+// its tile of rows; the last CTA to finish (ticket) turns the tile totals into their
+// exclusive prefix in place, so PE[k] = local[k-1] + tile_pre[(k-1) / kScanTile].
 __global__ void __launch_bounds__(256) k_block_scan(const unsigned long long* __restrict__ hist, int m,
                                                     const uint8_t* __restrict__ state, int W,
                                                     unsigned long long* __restrict__ local,
-                                                    unsigned long long* __restrict__ tile_tot) {
+                                                    unsigned long long* __restrict__ tile_tot,
+                                                    unsigned int* __restrict__ ticket) {
+  __shared__ bool last;
   pdl_launch_dependents();
   pdl_wait();  // the block's histogram launch is complete
   const DevStreamHeader* hd = reinterpret_cast<const DevStreamHeader*>(state);
@@ -1121,16 +1125,34 @@ __global__ void __launch_bounds__(256) k_block_scan(const unsigned long long* __
     if (k0 + j < R) local[size_t(k0 + j) * 256 + b] = s;  // inclusive: E[k0..k0+j]
   }
   tile_tot[size_t(blockIdx.x) * 256 + b] = s;
+  __threadfence();
+  __syncthreads();
+  if (b == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const int T = gridDim.x;
+  unsigned long long run = 0;
+  for (int j0 = 0; j0 < T; j0 += 8) {  // 8 independent loads in flight per round
+    unsigned long long t[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) t[j] = j0 + j < T ? __ldcg(tile_tot + size_t(j0 + j) * 256 + b) : 0ull;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j0 + j < T) {
+        tile_tot[size_t(j0 + j) * 256 + b] = run;  // exclusive prefix
+        run += t[j];
+      }
+  }
+  if (b == 0) *ticket = 0;  // zero again for the next block
 }
 
 // PE[k] (sum of E[0..k)) for bin b from the tile scan
-__device__ __forceinline__ unsigned long long pe_at(const unsigned long long* local, const unsigned long long* tile_tot,
+__device__ __forceinline__ unsigned long long pe_at(const unsigned long long* local, const unsigned long long* tile_pre,
                                                     int k, int b) {
   if (k <= 0) return 0ull;
-  const int last = k - 1, t = last / kScanTile;
-  unsigned long long s = __ldcg(local + size_t(last) * 256 + b);
-  for (int j = 0; j < t; ++j) s += __ldcg(tile_tot + size_t(j) * 256 + b);
-  return s;
+  const int last = k - 1;
+  return __ldcg(local + size_t(last) * 256 + b) + __ldcg(tile_pre + size_t(last / kScanTile) * 256 + b);
 }
 
 // one CTA (256 threads) per iteration of the block
@@ -1176,7 +1198,9 @@ __global__ void __launch_bounds__(256) k_block_commit(const __grid_constant__ Bl
                                                       const double* __restrict__ deg_log,
                                                       const uint32_t* __restrict__ argmax_in,
                                                       int32_t* __restrict__ kind_log,
-                                                      unsigned long long* __restrict__ ns_log) {
+                                                      unsigned long long* __restrict__ ns_log,
+                                                      unsigned long long* __restrict__ decision) {
+  pdl_launch_dependents();  // the next block's histogram does not touch the state
   pdl_wait();  // every iteration's fold is done (and with it the histogram and the scan)
   DevStreamHeader* hd = reinterpret_cast<DevStreamHeader*>(state);
   unsigned long long* acc = reinterpret_cast<unsigned long long*>(state + sizeof(DevStreamHeader));
@@ -1199,29 +1223,48 @@ __global__ void __launch_bounds__(256) k_block_commit(const __grid_constant__ Bl
       slot = slot + 1 == W ? 0 : slot + 1;
     }
   }
+  __shared__ double s_deg[kBlockMaxIter];
+  __shared__ uint32_t s_am[kBlockMaxIter];
+  __shared__ int32_t s_kind[kBlockMaxIter];
+  __shared__ unsigned long long s_now;
+  for (int i = b; i < bm.n_iter; i += blockDim.x) {  // independent loads, then a serial pass in smem
+    s_deg[i] = __ldcg(deg_log + bm.first_iteration + i);
+    s_am[i] = argmax_in[i];
+  }
   __syncthreads();
   if (b == 0) {
     uint32_t kind = hd->kind, hot = hd->hot;
     double dd = hd->decided_degeneracy;
-    const unsigned long long now = globaltimer_ns();
+    s_now = globaltimer_ns();
     for (int i = 0; i < bm.n_iter; ++i) {
       const int it = bm.first_iteration + i;
-      kind_log[it] = int32_t(kind);
-      if (ns_log) ns_log[it] = now;
+      s_kind[i] = int32_t(kind);
       if (((it + 1) % recompute_every) == 0) {  // decision for the next iteration (lag 1)
-        const double frac = deg_log[it];
+        const double frac = s_deg[i];
         kind = frac >= threshold ? HS_KIND_ADAPTIVE : HS_KIND_NAIVE;
-        hot = argmax_in[i];
+        hot = s_am[i];
         dd = frac;
       }
     }
     hd->kind = kind;
     hd->hot = hot;
     hd->decided_degeneracy = dd;
+    if (decision) {  // the decision in force after this block, for the host (mapped memory)
+      volatile unsigned long long* dv = decision;
+      dv[1] = (unsigned long long)kind | ((unsigned long long)hot << 32);
+      dv[2] = __double_as_longlong(dd);
+      __threadfence_system();
+      dv[0] = (unsigned long long)(bm.first_iteration + bm.n_iter);  // written last: the block's stamp
+    }
     const int ev = max(0, R - W);
     hd->head = uint32_t((uint32_t(head) + uint32_t(ev)) % uint32_t(W));
     hd->count = uint32_t(min(W, R));
     hd->chunks_seen += uint64_t(m);
+  }
+  __syncthreads();
+  for (int i = b; i < bm.n_iter; i += blockDim.x) {
+    kind_log[bm.first_iteration + i] = s_kind[i];
+    if (ns_log) ns_log[bm.first_iteration + i] = s_now;
   }
 }
 
@@ -1977,6 +2020,118 @@ int hs_stream_step(const uint8_t* d_data, const uint64_t* h_begin, const uint64_
                                      reinterpret_cast<uint8_t*>(d_state), window_size, threshold, decide, iteration,
                                      d_deg_log, d_div_log, d_kind_log,
                                      reinterpret_cast<unsigned long long*>(d_ns_log));
+  if (e != cudaSuccess) return fold(e);
+  return fold(cudaGetLastError());
+}
+
+// workspace of hs_stream_block: [scan ticket][argmax u32 x kBlockMaxIter][histogram
+// tickets + rows (hs_workspace_bytes(256))][local prefix (W + max_chunks) x 256 u64]
+// [tile totals -> their exclusive prefix]; zeroed once, every block leaves its tickets zero
+constexpr size_t kBlockHead = 16 + kBlockMaxIter * 4;  // scan ticket (16 B), argmax u32 per iteration
+size_t hs_stream_block_ws_bytes(int window_size, int max_chunks) {
+  if (window_size < 1 || max_chunks < 1 || max_chunks > kBlockMaxChunks) return 0;
+  const size_t rows = size_t(window_size) + size_t(max_chunks);
+  const size_t tiles = (rows + kScanTile - 1) / kScanTile;
+  return kBlockHead + ws_bytes_for(kMaxSeg) + rows * 256 * 8 + tiles * 256 * 8;
+}
+
+int hs_stream_block(const uint8_t* d_data, const uint64_t* h_begin, const uint64_t* h_end, int nseg,
+                    const int32_t* h_iter_chunks, int n_iter, void* d_state, int window_size, double threshold,
+                    int recompute_every, int first_iteration, int hot_bin, uint64_t* d_out, double* d_deg_log,
+                    double* d_div_log, int32_t* d_kind_log, uint64_t* d_ns_log, uint64_t* h_decision,
+                    void* d_ws, size_t ws_bytes, void* stream) {
+  if (!d_state || window_size < 1 || nseg < 1 || nseg > kBlockMaxChunks || n_iter < 1 || n_iter > kBlockMaxIter ||
+      recompute_every < 1 || first_iteration < 0 || !d_out || !d_deg_log || !d_div_log || !d_kind_log || !h_begin ||
+      !h_end || !h_iter_chunks || hot_bin > 255)
+    return HS_ERR_INVALID_ARG;
+  if (!(threshold > 0.0 && threshold < 1.0)) return HS_ERR_INVALID_ARG;
+  const size_t need = hs_stream_block_ws_bytes(window_size, nseg);
+  if (!d_ws || ws_bytes < need) return HS_ERR_WORKSPACE;
+  BlockMap bm;
+  bm.n_iter = n_iter;
+  bm.m = nseg;
+  bm.c0_unused = 0;
+  bm.first_iteration = first_iteration;
+  int c = 0;
+  for (int i = 0; i < n_iter; ++i) {
+    if (h_iter_chunks[i] < 0) return HS_ERR_INVALID_ARG;
+    c += h_iter_chunks[i];
+    bm.end_chunk[i] = c;
+  }
+  if (c != nseg) return HS_ERR_INVALID_ARG;
+  uint64_t total = 0;
+  for (int s = 0; s < nseg; ++s) {
+    if (h_end[s] < h_begin[s]) return HS_ERR_INVALID_ARG;
+    if ((h_begin[s] & 3) || (h_end[s] & 3)) return HS_ERR_ALIGNMENT;
+    total += h_end[s] - h_begin[s];
+  }
+  if (reinterpret_cast<uintptr_t>(d_data) & 3) return HS_ERR_ALIGNMENT;
+  if ((reinterpret_cast<uintptr_t>(d_out) | reinterpret_cast<uintptr_t>(d_state) |
+       reinterpret_cast<uintptr_t>(d_ws)) & 15)
+    return HS_ERR_ALIGNMENT;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  DevInfo di;
+  int rc = dev_info(di);
+  if (rc != HS_OK) return rc;
+  unsigned long long* dec = nullptr;
+  if (h_decision) {  // page-locked host memory, written by the commit kernel
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, h_decision) != cudaSuccess || a.type != cudaMemoryTypeHost ||
+        a.devicePointer == nullptr) {
+      cudaGetLastError();
+      return HS_ERR_INVALID_ARG;
+    }
+    dec = reinterpret_cast<unsigned long long*>(a.devicePointer);
+  }
+  uint8_t* ws = reinterpret_cast<uint8_t*>(d_ws);
+  unsigned int* scan_ticket = reinterpret_cast<unsigned int*>(ws);
+  uint32_t* argmax = reinterpret_cast<uint32_t*>(ws + 16);
+  uint8_t* hist_ws = ws + kBlockHead;
+  const size_t rows = size_t(window_size) + size_t(nseg);
+  unsigned long long* local = reinterpret_cast<unsigned long long*>(hist_ws + ws_bytes_for(kMaxSeg));
+  unsigned long long* tile_tot = local + rows * 256;
+  if (total == 0) {
+    cudaError_t e = cudaMemsetAsync(d_out, 0, size_t(nseg) * 256 * sizeof(uint64_t), st);
+    if (e != cudaSuccess) return fold(e);
+  } else {
+    // One histogram call for the whole block, chained behind the previous block's commit
+    // (input contract as hs_stream_step). hot_bin >= 0: the register path for that bin
+    // (the host's lagged view of the device's ADAPTIVE decision); counts are identical.
+    Tickets tk{reinterpret_cast<unsigned int*>(hist_ws),
+               reinterpret_cast<unsigned long long*>(hist_ws + kTicketBytes)};
+    PatternParams pp{};
+    pp.hot_bin = hot_bin >= 0 ? hot_bin : 0;
+    pp.hot_unique = hot_bin >= 0;
+    pp.total_slots = 256;
+    bool wait_first = false;
+    rc = launch_segments(d_data, h_begin, h_end, 0, nseg, hot_bin >= 0 ? HS_KIND_ADAPTIVE : HS_KIND_NAIVE,
+                         HS_IMPL_LANE, &pp, reinterpret_cast<unsigned long long*>(d_out), st, di, tk, 0, false,
+                         wait_first);
+    if (rc != HS_OK) return rc;
+  }
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const auto* hist = reinterpret_cast<const unsigned long long*>(d_out);
+  cfg.gridDim = dim3(unsigned((rows + kScanTile - 1) / kScanTile));
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_block_scan, hist, nseg, reinterpret_cast<const uint8_t*>(d_state),
+                                     window_size, local, tile_tot, scan_ticket);
+  if (e != cudaSuccess) return fold(e);
+  cfg.gridDim = dim3(unsigned(n_iter));
+  e = cudaLaunchKernelEx(&cfg, k_block_fold, bm, reinterpret_cast<uint8_t*>(d_state), window_size,
+                         (const unsigned long long*)local, (const unsigned long long*)tile_tot, d_deg_log, d_div_log,
+                         argmax);
+  if (e != cudaSuccess) return fold(e);
+  cfg.gridDim = dim3(1);
+  e = cudaLaunchKernelEx(&cfg, k_block_commit, bm, hist, reinterpret_cast<uint8_t*>(d_state), window_size, threshold,
+                         recompute_every, (const unsigned long long*)local, (const unsigned long long*)tile_tot,
+                         (const double*)d_deg_log, (const uint32_t*)argmax, d_kind_log,
+                         reinterpret_cast<unsigned long long*>(d_ns_log), dec);
   if (e != cudaSuccess) return fold(e);
   return fold(cudaGetLastError());
 }
