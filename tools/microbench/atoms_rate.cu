@@ -5,8 +5,8 @@
 //                4 bytes: PRMT + IMAD + ATOMS per byte, no global loads at all
 //   atoms_lds    the same addresses, LDS instead of ATOMS (the MIO pipe without atomics)
 //   k_lane_like  k_lane's inner loop over 1 GiB of HBM (LDG.128 + 16 x (PRMT+IMAD+ATOMS))
-// Each reports warp-instructions per SM clock from clock64 (per CTA, averaged) and the
-// achieved bytes/s; run for ~3 s each with NVML sampling SM clock and power alongside.
+// Each reports warp-ATOMS per SM per clock (rate / 148 / NVML SM clock) and the
+// bytes/s-equivalent (16 B per 16 ATOMS); run for ~3 s each with NVML sampling SM clock and power alongside.
 // build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -o ar atoms_rate.cu -lnvidia-ml
 #include <cstdio>
 #include <cstdint>
@@ -61,9 +61,9 @@ __global__ void __launch_bounds__(1024, 2) k_lane_like(const uint4* in, size_t n
   __syncthreads();
   const uint32_t tb = (uint32_t)__cvta_generic_to_shared(h) + (threadIdx.x & 31) * 4;
   const unsigned long long t0 = clock64();
-  const size_t per = nvec / gridDim.x, v0 = per * blockIdx.x;
+  const size_t per = (nvec / gridDim.x) / 4096 * 4096, v0 = per * blockIdx.x;  // whole rounds of 4 vectors/thread
   const uint4* p = in + v0 + threadIdx.x;
-  const size_t n = per / blockDim.x;
+  const size_t n = per / blockDim.x;  // vectors per thread, a multiple of 4
   uint4 A[2], B[2];
   A[0] = ldg_stream(p); A[1] = ldg_stream(p + 1024);
   auto word = [&](uint32_t x) {
@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(1024, 2) k_lane_like(const uint4* in, size_t n
     sh_inc(tb + (byte_of(x, 2) << 7)); sh_inc(tb + (byte_of(x, 3) << 7));
   };
   auto vec = [&](const uint4& v) { word(v.x); word(v.y); word(v.z); word(v.w); };
-  for (size_t j = 0; j + 2 <= n; j += 4) {
+  for (size_t j = 0; j + 4 <= n; j += 4) {
     B[0] = ldg_stream(p + 2048); B[1] = ldg_stream(p + 3072);
     vec(A[0]); vec(A[1]);
     if (j + 4 < n) { A[0] = ldg_stream(p + 4096); A[1] = ldg_stream(p + 5120); }
@@ -139,10 +139,11 @@ int main() {
     cudaEventSynchronize(e1);
     float ms; cudaEventElapsedTime(&ms, e0, e1);
     unsigned long long c; cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
-    const double cyc_per_cta = double(c) / (20.0 * grid);
-    const double ipc = instr_per_launch / grid * 2 / cyc_per_cta;  // 2 CTAs per SM
-    printf("%-12s cold: %.3f ms/launch, %.3f warp-instr per SM clock, %.0f GB/s-equivalent\n", name, ms / 20, ipc,
-           bytes_per_launch / (ms / 20 * 1e-3) / 1e9);
+    unsigned clk = 0;
+    { nvmlDevice_t d; nvmlInit(); nvmlDeviceGetHandleByIndex(0, &d); nvmlDeviceGetClockInfo(d, NVML_CLOCK_SM, &clk); }
+    const double per_s = instr_per_launch / (ms / 20 * 1e-3);
+    printf("%-12s cold: %.3f ms/launch, %.3f warp-ATOMS per SM clock (at %u MHz), %.0f GB/s-equivalent\n", name,
+           ms / 20, per_s / sms / (clk * 1e6), clk, bytes_per_launch / (ms / 20 * 1e-3) / 1e9);
     // sustained: ~3 s with NVML sampling
     Sampler s; s.start();
     cudaMemset(cyc, 0, 8);
@@ -158,17 +159,19 @@ int main() {
     cudaEventSynchronize(e1);
     cudaEventElapsedTime(&ms, e0, e1);
     cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
-    const double cyc2 = double(c) / (double(n) * grid);
-    printf("  %-12s sustained: %.3f ms/launch, %.3f warp-instr per SM clock, %.0f GB/s-equivalent\n", name,
-           ms / n, instr_per_launch / grid * 2 / cyc2, bytes_per_launch / (ms / n * 1e-3) / 1e9);
     s.finish(name);
+    double mhz = 0;
+    for (size_t i = s.mhz.size() / 3; i < s.mhz.size(); ++i) mhz += s.mhz[i];
+    mhz /= double(s.mhz.size() - s.mhz.size() / 3);
+    printf("  %-12s sustained: %.3f ms/launch, %.3f warp-ATOMS per SM clock, %.0f GB/s-equivalent\n", name,
+           ms / n, instr_per_launch / (ms / n * 1e-3) / sms / (mhz * 1e6), bytes_per_launch / (ms / n * 1e-3) / 1e9);
   };
   const int iters = 2048;
   // per launch: grid*32 warps * iters * 16 ATOMS
   const double synth_instr = double(grid) * 32 * iters * 16, synth_bytes = double(grid) * 1024 * iters * 16;
   run("atoms_only", [&] { k_synth<0><<<grid, 1024>>>(iters, cyc, sink); }, synth_instr, synth_bytes);
   run("atoms_lds", [&] { k_synth<1><<<grid, 1024>>>(iters, cyc, sink); }, synth_instr, synth_bytes);
-  run("k_lane_like", [&] { k_lane_like<<<grid, 1024>>>(in, nvec, cyc, sink); }, double(bytes) / 32,
-      double(bytes));
+  const double kb = double((nvec / grid) / 4096 * 4096) * grid * 16;  // bytes the kernel reads
+  run("k_lane_like", [&] { k_lane_like<<<grid, 1024>>>(in, nvec, cyc, sink); }, kb / 32, kb);
   return 0;
 }
