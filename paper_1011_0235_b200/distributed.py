@@ -65,6 +65,27 @@ def as_uint64(counts) -> np.ndarray:
     return counts.detach().cpu().numpy().view(np.uint64).copy()
 
 
+class _StdoutToStderr:
+    """fd-level redirect of stdout into stderr: NCCL/c10d print their banner ("NCCL
+    version ...") from C at communicator creation, and the bench's stdout must carry
+    exactly one JSON line."""
+
+    def __enter__(self):
+        import sys
+
+        sys.stdout.flush()
+        self._saved = os.dup(1)
+        os.dup2(2, 1)
+        return self
+
+    def __exit__(self, *exc):
+        import sys
+
+        sys.stdout.flush()
+        os.dup2(self._saved, 1)
+        os.close(self._saved)
+
+
 def init_process_group(backend: str | None = None, device=None):
     """One process per GPU (torchrun environment): initialise torch.distributed, bind the
     rank's device, create the communicator eagerly with a 2 KiB warm-up allreduce, and
@@ -79,17 +100,18 @@ def init_process_group(backend: str | None = None, device=None):
     if backend is None:
         backend = "nccl" if torch.cuda.is_available() else "gloo"
     t0 = time.perf_counter()
-    if not dist.is_initialized():
-        if backend == "nccl":
-            torch.cuda.set_device(local if device is None else device)
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local if device is None else device))
-        else:
-            dist.init_process_group(backend)
-    dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
-    warm = torch.zeros(BINS, dtype=torch.int64, device=dev)
-    dist.all_reduce(warm)
-    if dev.type == "cuda":
-        torch.cuda.synchronize(dev)
+    with _StdoutToStderr():
+        if not dist.is_initialized():
+            if backend == "nccl":
+                torch.cuda.set_device(local if device is None else device)
+                dist.init_process_group("nccl", device_id=torch.device("cuda", local if device is None else device))
+            else:
+                dist.init_process_group(backend)
+        dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
+        warm = torch.zeros(BINS, dtype=torch.int64, device=dev)
+        dist.all_reduce(warm)
+        if dev.type == "cuda":
+            torch.cuda.synchronize(dev)
     msg = (f"[hs.distributed] rank {dist.get_rank()}/{dist.get_world_size()} backend={dist.get_backend()} "
            f"device={dev} communicator ready in {(time.perf_counter() - t0) * 1e3:.1f} ms")
     log.info(msg)
