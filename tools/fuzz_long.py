@@ -2,7 +2,9 @@
 6 GiB device buffer: random segment counts (1-600), sizes (0 B - 2.5 GiB, word
 multiples), overlapping offsets, every impl and kind, hot-bin hints, workspaces for
 64/256/1000 segments or none, and the blocking entry with page-locked and pageable
-result buffers. Runs for SECONDS; prints one line per trial class and a summary.
+result buffers; round 2: merged outputs (HS_KIND_FLAG_MERGE: one row = the sum of
+the segments) and chained calls (HS_KIND_FLAG_CHAINED). Runs for SECONDS; prints one
+line per trial class and a summary.
 usage: python tools/fuzz_long.py [SECONDS]"""
 import os
 import sys
@@ -53,6 +55,11 @@ while time.time() < t_end:
     ws_key = rng.choice([0, 64, 256, 1000])
     ws = wss.get(int(ws_key))
     entry = rng.choice(["batched", "sync_pinned", "sync_pageable"])
+    merge = rng.random() < 0.3
+    if merge:
+        kind |= N.HS_KIND_FLAG_MERGE
+    if entry == "batched" and rng.random() < 0.5:
+        kind |= N.HS_KIND_FLAG_CHAINED  # the previous kernel on the stream is ours (or the bincounts)
     out = torch.full((nseg, 256), -1, dtype=torch.int64, device="cuda")
     args = (buf.data_ptr(), N.u64p(b0), N.u64p(b1), nseg, kind, impl, N.i64p(pat.offset), N.i64p(pat.count),
             960, 8, out.data_ptr())
@@ -72,6 +79,8 @@ while time.time() < t_end:
     for s in range(nseg):
         if sizes[s]:
             want[s] = torch.bincount(buf[int(b0[s]):int(b1[s])], minlength=256).cpu().numpy().astype(np.uint64)
+    if merge:  # one row: the sum of every segment
+        got, want = got[:1], want.sum(axis=0, dtype=np.uint64)[None, :]
     ok = np.array_equal(got, want)
     if ws is not None:
         ok = ok and not ws.any().item()
@@ -79,7 +88,7 @@ while time.time() < t_end:
     bytes_total += int(sizes.sum())
     if not ok:
         bad = [s for s in range(nseg) if not np.array_equal(got[s], want[s])]
-        print(f"MISMATCH trial {trials}: nseg {nseg} impl {impl} kind {kind} ws {ws_key} entry {entry} "
+        print(f"MISMATCH trial {trials}: nseg {nseg} impl {impl} kind {kind:#x} ws {ws_key} entry {entry} "
               f"bad segments {bad[:10]} sizes {[int(sizes[s]) for s in bad[:5]]}", flush=True)
         raise SystemExit(1)
     if trials % 25 == 0:
