@@ -95,10 +95,17 @@ int hs_device_query(int device, int* sm_count, int* smem_optin, int* l2_bytes);
 int hs_validate_pattern(const int64_t* h_offset, const int64_t* h_count,
                         int64_t total_slots, int64_t cap);
 
-/* Device workspace of hs_histogram_batched / hs_stream_step: 1 KB of tickets plus one
- * 2 KB accumulator row per segment of a launch, for launches of up to nseg segments
- * (clamped to [64, 256]). A workspace sized for n segments makes the call launch groups
- * of n segments; hs_stream_step needs at least hs_workspace_bytes(64). */
+/* Device workspace of hs_histogram_batched / hs_stream_step: a HS_WS_HEAD_BYTES header
+ * (a u64 call counter, u32 drained[HS_WS_SLOTS], u32 finalized[HS_WS_SLOTS]) and
+ * HS_WS_SLOTS call slots, each 1 KB of tickets plus one 2 KB accumulator row per segment
+ * of a launch, for launches of up to nseg segments (clamped to [64, 256]). Consecutive
+ * calls count into consecutive slots, so only the CTAs that store a call's output wait
+ * for the previous call on the stream. A workspace sized for n segments makes the call
+ * launch groups of n segments; hs_stream_step needs at least hs_workspace_bytes(64).
+ * Zero it once; calls leave every slot zero again and advance the header's counters.
+ * 16-byte aligned. */
+#define HS_WS_HEAD_BYTES 384
+#define HS_WS_SLOTS 4
 size_t hs_workspace_bytes(int nseg);
 
 /*

@@ -49,7 +49,17 @@ namespace {
 
 constexpr int kMaxSeg = 256;         // segments per launch (SegParams ~6.5 KB: large kernel params)
 constexpr int kMaxSegEngine = 64;    // per hs_stream_step batch (the fold stages it in shared memory)
-constexpr size_t kTicketBytes = 1024;  // workspace head: kMaxSeg u32 tickets
+constexpr size_t kTicketBytes = 1024;  // per call slot: kMaxSeg u32 tickets
+// Ticketed workspace = [header][kCallSlots rotating slots + 1 serial slot, each tickets +
+// accumulator rows]: see WsHeader.
+#ifndef HS_CALL_SLOTS
+#define HS_CALL_SLOTS HS_WS_SLOTS
+#endif
+constexpr int kCallSlots = HS_CALL_SLOTS;
+constexpr size_t kWsHeadBytes = HS_WS_HEAD_BYTES;
+// Every rotating call adds exactly kArrive to the header's call counter (claim_slot);
+// grids must stay below it.
+constexpr unsigned long long kArrive = 4096;
 constexpr uint64_t kBigCap = 1ull << 30;  // u32 per-warp counters: far from wrapping
 // CTA ranges are whole multiples of 4 KiB of the launch's concatenated range: with
 // ranges cut at word granularity (1 GiB over 296 CTAs = 3,627,504 bytes each) a warp's
@@ -327,12 +337,6 @@ __device__ __forceinline__ EachVec<U, VecFn> each_vec(VecFn& f) { return EachVec
 #define HS_LANE_THREADS 1024
 #define HS_LANE_BLOCKS 2
 #endif
-// How a call's first launch (wait_first) orders itself behind its stream predecessor:
-// 0 = PDL launch, trigger dependents at entry, then griddepcontrol.wait before loading;
-// 1 = PDL launch, wait first, then trigger; 2 = no PDL attribute (plain stream order).
-#ifndef HS_FIRST_LAUNCH
-#define HS_FIRST_LAUNCH 1
-#endif
 constexpr int kLaneThreads = HS_LANE_THREADS;
 constexpr int kLaneBlocks = HS_LANE_BLOCKS;
 constexpr int kLaneHotThreads = 768;
@@ -340,25 +344,113 @@ constexpr int kLaneMinBlocks = 2;  // HOT form
 constexpr uint32_t kLaneArrayBytes = 256 * 32 * 4;
 
 // Ticketed output (single launch, no memset): CTAs RED their counts for launch-local
-// segment s into a workspace accumulator row acc[s] that is zero between launches;
-// after a fence each CTA takes a ticket, and the last CTA to finish segment s takes
-// the row with atomicExch(.., 0) (reading and re-zeroing it), stores out[s] and
-// resets the ticket. Tail work is O(256) whatever the number of CTAs.
+// segment s into an accumulator row acc[s] of a workspace slot (zero between calls);
+// after a fence each CTA takes a ticket, and the last CTA to finish segment s takes the
+// row with atomicExch(.., 0) (reading and re-zeroing it), stores out[s] and resets the
+// ticket. Tail work is O(256) whatever the number of CTAs.
+//
+// Two ways a call gets its slot (the workspace header, WsHeader):
+//  * serial (large or multi-launch calls): the slot after the rotating ones; every CTA
+//    waits for the previous launch on the stream to complete (griddepcontrol.wait)
+//    before its first RED, so calls -- and the launches of one call -- use it in turn.
+//  * rotating (single-launch calls up to kRotateMaxBytes): consecutive such calls take
+//    slots 0, 1, .., K-1, 0, .. Each CTA arrives on the call counter before it lets the
+//    next launch in, so the counter orders the calls; a call's CTAs RED into their slot
+//    once every earlier call on it has drained it (drained[slot] == the call's epoch),
+//    and the call's last finalization releases it (drained[slot] = epoch + 1) -- before
+//    waiting for the predecessor. Only the CTAs that store the output wait for the
+//    previous launch (the output is what a call shares with it); the rest of the call
+//    streams, flushes and exits while earlier calls drain. A small call's time is then
+//    one completion latency, not its predecessor's whole tail: 1 MiB chained calls 4.3 ->
+//    2.3 us. For larger launches the arrival (an atomic round trip before the trigger) on
+//    the launch-to-launch path costs more than the overlap gains (48 MiB: 8.7 -> 10.3 us),
+//    so they stay serial (profiles/r2_call_slots.txt).
+//    Deadlock-free: a launch starts only after every CTA of the launch before it has
+//    arrived, so when a CTA spins on its slot, all CTAs of earlier calls are resident or
+//    done, and an earlier call's release waits on nothing later.
+struct WsHeader {  // one 128-byte line per field: the arrivals do not contend with the probes
+  unsigned long long calls;            // kArrive per rotating call
+  unsigned long long pad0[15];
+  unsigned int drained[kCallSlots];    // calls that have released slot j
+  unsigned int pad1[32 - kCallSlots];
+  unsigned int finalized[kCallSlots];  // finalizations of the current call on slot j
+  unsigned int pad2[32 - kCallSlots];
+};
+static_assert(sizeof(WsHeader) <= kWsHeadBytes, "workspace header");
+
 struct Tickets {
-  unsigned int* ticket;          // [kMaxSeg], zero on entry and on exit
-  unsigned long long* acc;       // [kMaxSeg][256], zero on entry and on exit
+  WsHeader* hdr;       // nullptr: untracked output (memset + RED into d_out)
+  uint8_t* slots;      // slot j at slots + j * slot_bytes: [tickets][rows]; j = kCallSlots: serial
+  uint32_t slot_bytes;
+  uint32_t rotate;     // this call takes a rotating slot (one launch)
+  uint32_t nfinal;     // segment finalizations of the call (rotating: releases the slot)
 };
 
+// The slot a CTA counts into
+struct SlotView {
+  unsigned int* ticket;
+  unsigned long long* acc;
+  uint32_t slot, epoch, probe;  // probe: drained[slot] as read after the claim
+};
+
+__device__ __forceinline__ unsigned int ld_relaxed_u32(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned int* p, unsigned int v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void set_slot(const Tickets& tk, uint32_t slot, SlotView& sv) {
+  sv.slot = slot;
+  uint8_t* base = tk.slots + size_t(slot) * tk.slot_bytes;
+  sv.ticket = reinterpret_cast<unsigned int*>(base);
+  sv.acc = reinterpret_cast<unsigned long long*>(base + kTicketBytes);
+}
+
+// thread 0 of every CTA of a rotating call, before it triggers: arrive (CTA 0 adds
+// kArrive - grid + 1, the others 1, so the counter moves by kArrive per call and the
+// value returned to any CTA of the call, over kArrive, is the call's number n)
+__device__ __forceinline__ void claim_slot(const Tickets& tk, SlotView& sv) {
+  const unsigned long long n =
+      atomicAdd(&tk.hdr->calls, blockIdx.x == 0 ? kArrive - gridDim.x + 1 : 1ull) / kArrive;
+  set_slot(tk, uint32_t(n % kCallSlots), sv);
+  sv.epoch = uint32_t(n / kCallSlots);
+}
+
+// read once the next launch is let in, looked at by the first flush: by then it is back
+__device__ __forceinline__ void probe_slot(const Tickets& tk, SlotView& sv) {
+  sv.probe = ld_relaxed_u32(&tk.hdr->drained[sv.slot]);
+}
+
+// thread 0, before the CTA's first RED into a rotating slot: every earlier call on the
+// slot has released it (the probe saw the release store, with the fence making it an
+// acquire, or the acquire loop does)
+__device__ __forceinline__ void await_slot(const Tickets& tk, SlotView& sv) {
+  if (sv.probe == sv.epoch) {
+    __threadfence();
+    return;
+  }
+  while (ld_acquire_u32(&tk.hdr->drained[sv.slot]) != sv.epoch) __nanosleep(64);
+  sv.probe = sv.epoch;
+}
 
 // Adds the CTA's counters into dst[256] (the output row, or the segment's accumulator
 // row of a ticketed launch) and re-zeroes them unless this was the CTA's last piece:
 // 4 threads per bin, each summing 8 of the bin's 32 lane words (staggered: conflict
 // free), shuffle-combined. No fence here: the fence and the tickets are taken once per
 // CTA at the end (lane_tickets), after all of its flushes.
-__device__ __forceinline__ void lane_flush(uint32_t sbase, unsigned long long* __restrict__ dst, bool rezero) {
+__device__ __forceinline__ void lane_flush(uint32_t sbase, unsigned long long* __restrict__ dst, bool rezero,
+                                           bool wait_pred) {
   compiler_fence();
   __syncthreads();
-  pdl_wait();  // the previous launch on this stream may still own the workspace / outputs
+  if (wait_pred) pdl_wait();  // the previous launch may still own the rows (see k_lane)
   for (uint32_t t = threadIdx.x; t < 1024; t += blockDim.x) {
     const uint32_t b = t >> 2, sub = t & 3;
     uint32_t v = 0;
@@ -377,12 +469,29 @@ __device__ __forceinline__ void lane_flush(uint32_t sbase, unsigned long long* _
   __syncthreads();
 }
 
+// The rotating call's last finalization releases its slot
+__device__ __forceinline__ void release_slot(const Tickets& tk, const SlotView& sv, int m) {
+  if (threadIdx.x != 0) return;
+  if (unsigned(m) == tk.nfinal) {  // the call's only finalizing CTA
+    st_release_u32(&tk.hdr->drained[sv.slot], sv.epoch + 1);
+    return;
+  }
+  __threadfence();
+  if (atomicAdd(&tk.hdr->finalized[sv.slot], unsigned(m)) + unsigned(m) == tk.nfinal) {
+    tk.hdr->finalized[sv.slot] = 0;
+    __threadfence();
+    st_release_u32(&tk.hdr->drained[sv.slot], sv.epoch + 1);
+  }
+}
+
 // End of a ticketed CTA that flushed segments [s_first, s_last] into their accumulator
 // rows: one fence, then a ticket per segment; the last CTA of a segment takes the row
 // with atomicExch(.., 0) (reading and re-zeroing it), stores the output row and resets
-// the ticket, so workspace and tickets are zero again when the launch ends.
-__device__ __forceinline__ void lane_tickets(const Tickets& tk, const SegParams& sp, int s_first, int s_last,
-                                          unsigned long long* __restrict__ out) {
+// the ticket, so the slot's rows and tickets are zero again when the call ends.
+// stage: the CTA's 32 KB counter array, free after its last flush (16 rows of u64[256])
+constexpr int kStageRows = 16;
+__device__ __forceinline__ void lane_tickets(const Tickets& tk, const SlotView& sv, const SegParams& sp, int s_first,
+                                          int s_last, unsigned long long* __restrict__ out, uint32_t* stage_words) {
   __shared__ int last_seg[kMaxSeg];
   __shared__ int n_last;
   if (sp.merge && !sp.merge_final) return;  // a later launch of the call finalizes the row
@@ -391,26 +500,50 @@ __device__ __forceinline__ void lane_tickets(const Tickets& tk, const SegParams&
   if (threadIdx.x == 0) {
     int m = 0;
     if (sp.merge) {
-      if (atomicAdd(tk.ticket + sp.acc_base, 1u) == sp.merge_ctas) last_seg[m++] = 0;
+      if (atomicAdd(sv.ticket + sp.acc_base, 1u) == sp.merge_ctas) last_seg[m++] = 0;
       s_last = -1;  // no per-segment tickets
     }
     for (int s = s_first; s <= s_last; ++s) {
       if (sp.vstart[s + 1] == sp.vstart[s]) continue;  // empty: no CTA owns it
       if ((sp.open_mask[s >> 5] >> (s & 31)) & 1) continue;  // finalized by a later launch
-      if (atomicAdd(tk.ticket + sp.acc_base + s, 1u) == sp.ctas_after_first[s]) last_seg[m++] = s;
+      if (atomicAdd(sv.ticket + sp.acc_base + s, 1u) == sp.ctas_after_first[s]) last_seg[m++] = s;
     }
     n_last = m;
   }
   __syncthreads();
   const int m = n_last;
-  if (m) {
-    __threadfence();
+  if (!m) return;
+  __threadfence();
+  // The output is what this call shares with its predecessor on the stream (the same
+  // buffer, or one the predecessor reads): it is stored only once that one is complete
+  // (griddepcontrol.wait; serial calls have waited before their first RED). A rotating
+  // slot is drained and released before that wait, so later calls can take it meanwhile.
+  if (tk.rotate && m <= kStageRows) {
+    unsigned long long* stage = reinterpret_cast<unsigned long long*>(stage_words);
     for (int k = 0; k < m; ++k) {
       const int s = last_seg[k];
       for (uint32_t b = threadIdx.x; b < 256; b += blockDim.x)
-        out[size_t(sp.out_base + s) * 256 + b] = atomicExch(tk.acc + size_t(sp.acc_base + s) * 256 + b, 0ull);
-      if (threadIdx.x == 0) tk.ticket[sp.acc_base + s] = 0;
+        stage[k * 256 + b] = atomicExch(sv.acc + size_t(sp.acc_base + s) * 256 + b, 0ull);
+      if (threadIdx.x == 0) sv.ticket[sp.acc_base + s] = 0;
     }
+    __syncthreads();
+    release_slot(tk, sv, m);
+    pdl_wait();
+    for (int k = 0; k < m; ++k)
+      for (uint32_t b = threadIdx.x; b < 256; b += blockDim.x)
+        out[size_t(sp.out_base + last_seg[k]) * 256 + b] = stage[k * 256 + b];
+    return;
+  }
+  pdl_wait();
+  for (int k = 0; k < m; ++k) {
+    const int s = last_seg[k];
+    for (uint32_t b = threadIdx.x; b < 256; b += blockDim.x)
+      out[size_t(sp.out_base + s) * 256 + b] = atomicExch(sv.acc + size_t(sp.acc_base + s) * 256 + b, 0ull);
+    if (threadIdx.x == 0) sv.ticket[sp.acc_base + s] = 0;
+  }
+  if (tk.rotate) {
+    __syncthreads();
+    release_slot(tk, sv, m);
   }
 }
 
@@ -418,9 +551,9 @@ __device__ __forceinline__ void lane_tickets(const Tickets& tk, const SegParams&
 // resident warps: the < U*T-vector remainder is counted first, so nothing but the
 // running 16-B pointer, a countdown and the column base is live across the main
 // double-buffered loop; compile-time stride.
-template <int U, bool HOT, int TH>
+template <int U, bool HOT, int TH, class Hook>
 __device__ __forceinline__ uint32_t lane_loop(const uint8_t* __restrict__ data, uint64_t a0, uint64_t a1,
-                                              uint32_t tb, uint32_t hot4) {
+                                              uint32_t tb, uint32_t hot4, Hook&& hook) {
   constexpr uint32_t T = TH;
   const uint32_t tid = threadIdx.x;
   uint32_t hotcnt = 0;
@@ -449,6 +582,7 @@ __device__ __forceinline__ uint32_t lane_loop(const uint8_t* __restrict__ data, 
 #pragma unroll
     for (int u = 0; u < U; ++u) A[u] = ldg_stream(q + u * T);
   }
+  hook();  // (the CTA's first piece: its start protocol, while the first loads are in flight)
   // invariant at the loop head: A holds batch 0 of the nfull batches left at q
   while (nfull >= 2) {
 #pragma unroll
@@ -481,9 +615,9 @@ __device__ __forceinline__ uint32_t lane_loop(const uint8_t* __restrict__ data, 
 // (Tried and rejected: verifying the hot bin on a per-CTA sample and switching between
 // the checked and the plain loop at run time -- both loops in one function exceed the
 // 32-register budget of 64 resident warps and the plain loop spills.)
-template <int U, bool HOT, int TH>
+template <int U, bool HOT, int TH, class Hook>
 __device__ __forceinline__ uint32_t lane_piece(const uint8_t* __restrict__ data, uint64_t p0, uint64_t p1,
-                                            uint32_t tb, uint32_t hot4) {
+                                            uint32_t tb, uint32_t hot4, Hook&& hook) {
   const uint32_t tid = threadIdx.x;
   auto word = [&](uint32_t w) {
     sh_inc(tb + (byte_of(w, 0) << 7));
@@ -496,7 +630,7 @@ __device__ __forceinline__ uint32_t lane_piece(const uint8_t* __restrict__ data,
   const uint64_t a1 = max(a0, ((base + p1) & ~uint64_t(15)) - base);
   if (p0 + 4ull * tid < a0) word(*reinterpret_cast<const uint32_t*>(data + p0 + 4ull * tid));
   if (a1 + 4ull * tid < p1) word(*reinterpret_cast<const uint32_t*>(data + a1 + 4ull * tid));
-  const uint32_t hotcnt = lane_loop<U, HOT, TH>(data, a0, a1, tb, hot4);
+  const uint32_t hotcnt = lane_loop<U, HOT, TH>(data, a0, a1, tb, hot4, hook);
   if (HOT && hotcnt) sh_add(tb + ((hot4 & 0xffu) << 7), hotcnt);
   return 0;
 }
@@ -520,15 +654,29 @@ __global__ void __launch_bounds__(TH, MB)
   __shared__ uint64_t pc_p0[kMaxSeg], pc_p1[kMaxSeg];
   __shared__ int pc_seg[kMaxSeg];
   __shared__ int pc_n;
+  __shared__ SlotView sv;
   HS_STAMP(0);
-#if HS_FIRST_LAUNCH == 1
+  // A call's first launch waits for its stream predecessor before loading (round 2 A/B,
+  // profiles/r2_first_launch_ab.txt: waiting first, then letting the next launch in, was
+  // the fastest safe order). A rotating call's CTAs let the next launch in only after
+  // arriving on the workspace's call counter (claim_slot), which orders the calls' slots.
   if (wait_first) pdl_wait();
-  pdl_launch_dependents();  // the next launch's CTAs may take SMs as ours retire
-#else
-  pdl_launch_dependents();  // the next launch's CTAs may take SMs as ours retire
-  if (wait_first) pdl_wait();
-#endif
+  const bool ticketed = tk.hdr != nullptr;
+  const bool rotating = ticketed && tk.rotate;
+  // A CTA counts as triggered once any of its threads has executed launch_dependents
+  // (tools/microbench/pdl_trigger.cu). Every thread triggering at entry lets the next
+  // launch in soonest (in the microbenchmark a lone thread's trigger took ~2 us longer to
+  // take effect); a rotating call's CTAs trigger from thread 0 only, after its arrival
+  // is back, so that every CTA of the call arrives before any CTA of the next one.
+  if (!rotating) pdl_launch_dependents();
   if (threadIdx.x == 0) {
+    if (rotating) {
+      claim_slot(tk, sv);
+      pdl_launch_dependents();
+      probe_slot(tk, sv);
+    } else if (ticketed) {
+      set_slot(tk, kCallSlots, sv);
+    }
     int n = 0;
     for_each_piece<~0ull>(sp, [&](int s, uint64_t p0, uint64_t p1) {
       pc_p0[n] = p0;
@@ -543,7 +691,7 @@ __global__ void __launch_bounds__(TH, MB)
   __syncthreads();
   const uint32_t tb = sbase + (threadIdx.x & 31) * 4;  // column base: bank == lane
   const uint32_t hot = uint32_t(hot_bin) & 0xff;
-  if (tk.ticket != nullptr && blockIdx.x == 0 && !sp.merge) {
+  if (ticketed && blockIdx.x == 0 && !sp.merge) {
     // ticketed launches have no memset: CTA 0 zeroes the empty segments' outputs
     bool any_empty = false;
     for (int s = 0; s < sp.nseg; ++s) any_empty |= sp.vstart[s + 1] == sp.vstart[s];
@@ -554,21 +702,24 @@ __global__ void __launch_bounds__(TH, MB)
           for (uint32_t b = threadIdx.x; b < 256; b += blockDim.x) out[size_t(sp.out_base + s) * 256 + b] = 0;
     }
   }
+  auto no_hook = []() {};
   // u32 columns: a column adds at most (CTA bytes)/32 <= 2^32, so one flush per
   // (CTA, segment) suffices -- required by the ticketed output
   const uint32_t hot4 = hot * 0x01010101u;
-  const bool ticketed = tk.ticket != nullptr;
   HS_STAMP(1);
   for (int i = 0; i < pc_n; ++i) {
-    lane_piece<U, HOT, TH>(data, pc_p0[i], pc_p1[i], tb, hot4);
+    lane_piece<U, HOT, TH>(data, pc_p0[i], pc_p1[i], tb, hot4, no_hook);
     HS_STAMP(2 + 2 * i);
     if (sp.merge && i + 1 < pc_n) continue;  // merged output: one flush per CTA
     const int r = seg_row(sp, pc_seg[i]);
-    lane_flush(sbase, ticketed ? tk.acc + size_t(sp.acc_base + r) * 256 : out + size_t(sp.out_base + r) * 256,
-               i + 1 < pc_n);
+    // a rotating call counts into its slot once the slot is free; a serial one once the
+    // previous launch on the stream is complete (and so, transitively, every earlier one)
+    if (rotating && threadIdx.x == 0) await_slot(tk, sv);  // lane_flush's barrier publishes it
+    lane_flush(sbase, ticketed ? sv.acc + size_t(sp.acc_base + r) * 256 : out + size_t(sp.out_base + r) * 256,
+               i + 1 < pc_n, ticketed && !rotating);
     HS_STAMP(3 + 2 * i);
   }
-  if (ticketed && pc_n > 0) lane_tickets(tk, sp, pc_seg[0], pc_seg[pc_n - 1], out);
+  if (ticketed && pc_n > 0) lane_tickets(tk, sv, sp, pc_seg[0], pc_seg[pc_n - 1], out, counters);
   HS_STAMP(15);
 }
 
@@ -795,7 +946,7 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneBlocks)
     if (lane == 0 && t) atomicAdd(sink, t);
     return;
   }
-  lane_flush(cbase, out, false);  // FULL: reduce_subbins + merge (u64 RED per bin)
+  lane_flush(cbase, out, false, false);  // FULL: reduce_subbins + merge (u64 RED per bin)
   if (threadIdx.x == 0 && vb < ve) atomicAdd(sink, (unsigned long long)(ve - vb));
 }
 
@@ -1540,7 +1691,8 @@ int launch_batch(const uint8_t* d_data, SegParams& sp, int kind, int impl, const
     // PDL overlaps a launch's ramp with the previous launch's tail (in the device
     // stream engine: with the previous iteration's one-CTA fold)
     cfg.attrs = attr;
-    cfg.numAttrs = (HS_FIRST_LAUNCH == 2 && wait_first) ? 0 : 1;  // mode 2: plain stream order
+    cfg.numAttrs = 1;
+    if (tk.hdr != nullptr && uint64_t(grid) >= kArrive) return HS_ERR_UNSUPPORTED;
     if (hot) {
       cfg.blockDim = dim3(kLaneHotThreads);
       e = cudaLaunchKernelEx(&cfg, k_lane<2, true, kLaneHotThreads, kLaneMinBlocks>, d_data, sp, hb, d_out, tk,
@@ -1586,7 +1738,7 @@ constexpr uint64_t kLaunchBytes = 1ull << 30;  // a word multiple, so every cut 
 
 int launch_segments(const uint8_t* d_data, const uint64_t* h_begin, const uint64_t* h_end, int s0, int ns,
                     int kind, int impl, const PatternParams* pp, unsigned long long* d_out, cudaStream_t st,
-                    const DevInfo& di, const Tickets& tk, int reserve_slots, bool latency, bool& wait_first,
+                    const DevInfo& di, Tickets& tk, int reserve_slots, bool latency, bool& wait_first,
                     bool merge = false, bool final_group = true) {
   uint64_t vs[kMaxSeg + 1];
   vs[0] = 0;
@@ -1668,10 +1820,13 @@ int hs_validate_pattern(const int64_t* h_offset, const int64_t* h_count, int64_t
   return validate(h_offset, h_count, total_slots, cap);
 }
 
-// [tickets: kMaxSeg u32 = 1 KB][accumulators: one 256 x u64 row per segment of a
-// launch]; zero it once after allocating -- every ticketed launch leaves it zero again.
-// A workspace sized for n segments lets launches take up to n (<= kMaxSeg) segments.
-constexpr size_t ws_bytes_for(int nseg) { return kTicketBytes + size_t(nseg) * 256 * sizeof(uint64_t); }
+// [header: call counter, drained[K], finalized[K]] then K call slots of [tickets: kMaxSeg
+// u32 = 1 KB][accumulators: one 256 x u64 row per segment of a launch]; zero it once
+// after allocating -- every call leaves its slot's tickets and rows zero again (the
+// header's counters advance). A workspace sized for n segments lets launches take up to
+// n (<= kMaxSeg) segments.
+constexpr size_t slot_bytes_for(int nseg) { return kTicketBytes + size_t(nseg) * 256 * sizeof(uint64_t); }
+constexpr size_t ws_bytes_for(int nseg) { return kWsHeadBytes + (kCallSlots + 1) * slot_bytes_for(nseg); }
 constexpr size_t kWorkspaceBytes = ws_bytes_for(kMaxSegEngine);  // the minimum accepted
 size_t hs_workspace_bytes(int nseg) {
   return nseg < 0 ? 0 : ws_bytes_for(std::max(kMaxSegEngine, std::min(nseg, kMaxSeg)));
@@ -1680,6 +1835,37 @@ size_t hs_workspace_bytes(int nseg) {
 }  // extern "C"
 
 namespace {
+// Ticket view of a caller workspace of ws_bytes (rows per slot: the launch group size)
+Tickets tickets_of(void* d_ws, size_t ws_bytes, int& rows) {
+  Tickets tk{};
+  const size_t per = (ws_bytes - kWsHeadBytes) / (kCallSlots + 1);
+  rows = int(std::min<size_t>(kMaxSeg, (per - kTicketBytes) / (256 * sizeof(uint64_t))));
+  tk.hdr = reinterpret_cast<WsHeader*>(d_ws);
+  tk.slots = reinterpret_cast<uint8_t*>(d_ws) + kWsHeadBytes;
+  tk.slot_bytes = uint32_t(slot_bytes_for(rows));
+  tk.rotate = 0;
+  tk.nfinal = 0;
+  return tk;
+}
+
+// A call over segments [s0, s0 + ns) of `total` bytes takes a rotating slot when it is one
+// launch of at most kRotateMaxBytes (see WsHeader); it then needs its finalization count.
+#ifndef HS_ROTATE_MAX_MIB
+#define HS_ROTATE_MAX_MIB 16
+#endif
+constexpr uint64_t kRotateMaxBytes = uint64_t(HS_ROTATE_MAX_MIB) << 20;
+void plan_call(Tickets& tk, const uint64_t* h_begin, const uint64_t* h_end, int s0, int ns, bool merge) {
+  if (tk.hdr == nullptr) return;
+  uint64_t total = 0;
+  uint32_t n = 0;
+  for (int i = s0; i < s0 + ns; ++i) {
+    total += h_end[i] - h_begin[i];
+    n += h_end[i] > h_begin[i];
+  }
+  tk.rotate = total > 0 && total <= kRotateMaxBytes;
+  tk.nfinal = merge ? 1 : n;
+}
+
 int histogram_batched(const uint8_t* d_data, const uint64_t* h_begin, const uint64_t* h_end, int nseg, int kind,
                       int impl, const int64_t* h_offset, const int64_t* h_count, int64_t total_slots, int64_t cap,
                       uint64_t* d_out, void* d_ws, size_t ws_bytes, void* stream, bool latency) {
@@ -1715,19 +1901,20 @@ int histogram_batched(const uint8_t* d_data, const uint64_t* h_begin, const uint
   if (impl == HS_IMPL_AUTO) impl = HS_IMPL_LANE;
   // LANE with a workspace: one launch per group of segments the workspace has rows for
   // (<= kMaxSeg), output written in-kernel; otherwise memset + RED, kMaxSeg per launch
-  Tickets tk{nullptr, nullptr};
+  Tickets tk{};
   int group = kMaxSeg;
   if (impl == HS_IMPL_LANE && d_ws != nullptr && ws_bytes >= kWorkspaceBytes && total > 0) {
-    tk.ticket = reinterpret_cast<unsigned int*>(d_ws);
-    tk.acc = reinterpret_cast<unsigned long long*>(reinterpret_cast<uint8_t*>(d_ws) + kTicketBytes);
-    group = int(std::min<size_t>(kMaxSeg, (ws_bytes - kTicketBytes) / (256 * sizeof(uint64_t))));
+    if (reinterpret_cast<uintptr_t>(d_ws) & 15) return HS_ERR_ALIGNMENT;
+    tk = tickets_of(d_ws, ws_bytes, group);
     if (merge) group = kMaxSeg;  // one accumulator row whatever the segment count
+    // a merged call over several groups finalizes once, in its last group: serial
+    if (merge && nseg <= group) plan_call(tk, h_begin, h_end, 0, nseg, true);
   } else {
     cudaError_t e = cudaMemsetAsync(d_out, 0, size_t(merge ? 1 : nseg) * 256 * sizeof(uint64_t), st);
     if (e != cudaSuccess) return fold(e);
   }
   if (total == 0) {
-    if (merge && tk.ticket != nullptr) return fold(cudaMemsetAsync(d_out, 0, 256 * sizeof(uint64_t), st));
+    if (merge && tk.hdr != nullptr) return fold(cudaMemsetAsync(d_out, 0, 256 * sizeof(uint64_t), st));
     return HS_OK;
   }
   // merged calls: the last group holding bytes finalizes the row
@@ -1738,11 +1925,12 @@ int histogram_batched(const uint8_t* d_data, const uint64_t* h_begin, const uint
     bool empty = true;
     for (int i = 0; i < ns; ++i) empty = empty && h_end[s0 + i] == h_begin[s0 + i];
     if (empty && merge) continue;
-    if (empty && tk.ticket != nullptr) {
+    if (empty && tk.hdr != nullptr) {
       cudaError_t e = cudaMemsetAsync(d_out + size_t(s0) * 256, 0, size_t(ns) * 256 * sizeof(uint64_t), st);
       if (e != cudaSuccess) return fold(e);
       continue;
     }
+    if (!merge) plan_call(tk, h_begin, h_end, s0, ns, false);  // each group is a call of its own
     rc = launch_segments(d_data, h_begin, h_end, s0, ns, kind, impl, have_pattern ? &pp : nullptr,
                          reinterpret_cast<unsigned long long*>(d_out), st, di, tk, 0, latency, wait_first, merge,
                          last_busy < s0 + ns);
@@ -1984,8 +2172,10 @@ int hs_stream_step(const uint8_t* d_data, const uint64_t* h_begin, const uint64_
   DevInfo di;
   int rc = dev_info(di);
   if (rc != HS_OK) return rc;
-  Tickets tk{reinterpret_cast<unsigned int*>(d_ws),
-             reinterpret_cast<unsigned long long*>(reinterpret_cast<uint8_t*>(d_ws) + kTicketBytes)};
+  if (reinterpret_cast<uintptr_t>(d_ws) & 15) return HS_ERR_ALIGNMENT;
+  int rows = 0;
+  Tickets tk = tickets_of(d_ws, ws_bytes, rows);
+  plan_call(tk, h_begin, h_end, 0, nseg, false);
   bool empty = total == 0;
   if (empty) {
     cudaError_t e = cudaMemsetAsync(d_out, 0, size_t(nseg) * 256 * sizeof(uint64_t), st);
@@ -2097,8 +2287,9 @@ int hs_stream_block(const uint8_t* d_data, const uint64_t* h_begin, const uint64
     // One histogram call for the whole block, chained behind the previous block's commit
     // (input contract as hs_stream_step). hot_bin >= 0: the register path for that bin
     // (the host's lagged view of the device's ADAPTIVE decision); counts are identical.
-    Tickets tk{reinterpret_cast<unsigned int*>(hist_ws),
-               reinterpret_cast<unsigned long long*>(hist_ws + kTicketBytes)};
+    int rows = 0;
+    Tickets tk = tickets_of(hist_ws, ws_bytes_for(kMaxSeg), rows);
+    plan_call(tk, h_begin, h_end, 0, nseg, false);
     PatternParams pp{};
     pp.hot_bin = hot_bin >= 0 ? hot_bin : 0;
     pp.hot_unique = hot_bin >= 0;

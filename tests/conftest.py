@@ -58,3 +58,17 @@ def cuda():
 
     _native.lib()
     return torch
+
+
+WS_HEAD_BYTES = 384  # include/hist256.h HS_WS_HEAD_BYTES: calls u64 @0, drained u32[4] @128, finalized @256
+WS_DRAINED = slice(128, 144)
+WS_FINALIZED = slice(256, 272)
+
+
+def ws_clean(ws) -> bool:
+    """A ticketed-histogram workspace between calls: every call slot (tickets and
+    accumulator rows) zero again and no finalization pending; the header's call
+    counter and per-slot drain counts advance and are not checked here."""
+    head = ws[:WS_HEAD_BYTES].cpu().numpy()
+    finalized = head[WS_FINALIZED]
+    return not ws[WS_HEAD_BYTES:].any().item() and not finalized.any()

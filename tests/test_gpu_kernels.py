@@ -8,6 +8,7 @@ import zlib
 
 import numpy as np
 import pytest
+from conftest import ws_clean
 
 import paper_1011_0235_b200 as hs
 from paper_1011_0235_b200 import _native as N
@@ -323,7 +324,7 @@ def test_ticketed_output_matches_atomic_output(cuda, oracle):
                 N.check(st, "hs_histogram_batched")
                 assert np.array_equal(out.cpu().numpy().view(np.uint64), want), (trial, kind, use_ws)
     # every launch leaves the workspace (tickets and accumulator rows) zero again
-    assert int(ws.sum().item()) == 0
+    assert ws_clean(ws)
 
 
 @pytest.mark.parametrize("p", [0.5, 0.99, 0.9995])
@@ -396,7 +397,7 @@ def test_graph_replay_ticketed(cuda, oracle):
             got = o.cpu().numpy().view(np.uint64)
             for k in range(3):
                 assert got[k].tolist() == parts[k].tolist()
-    assert not ws.any().item()
+    assert ws_clean(ws)
 
 
 @pytest.mark.parametrize("seed", range(4))
@@ -432,7 +433,7 @@ def test_fuzz_segment_layouts(cuda, seed):
         got = out.cpu().numpy().view(np.uint64)
         assert np.array_equal(got, want), (seed, trial, nseg, impl, kind, ws_seg)
         if ws_seg:
-            assert not ws.any().item()
+            assert ws_clean(ws)
 
 
 def test_concurrent_streams_separate_workspaces(cuda, oracle):
@@ -461,7 +462,7 @@ def test_concurrent_streams_separate_workspaces(cuda, oracle):
     for j in range(3):
         for k in range(5):
             assert np.array_equal(outs[j][k].cpu().numpy().view(np.uint64), wants[j]), (j, k)
-        assert not wss[j].any().item()
+        assert ws_clean(wss[j])
 
 
 def _sync_call(lib, d, begin, end, h_out, d_out, ws, impl=N.HS_IMPL_AUTO):

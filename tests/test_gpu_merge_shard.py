@@ -15,6 +15,7 @@ import socket
 
 import numpy as np
 import pytest
+from conftest import ws_clean
 
 import paper_1011_0235_b200 as hs
 from paper_1011_0235_b200 import _native as N
@@ -65,7 +66,7 @@ def test_merge_random_layouts(cuda, seed):
         if nseg > 1:  # only row 0 is written
             assert (out[1:] == -1).all().item()
         if use_ws:
-            assert not ws.any().item(), "workspace left non-zero"
+            assert ws_clean(ws), "workspace left non-zero"
 
 
 def test_merge_over_one_gib_and_all_empty(cuda, oracle):
@@ -83,7 +84,7 @@ def test_merge_over_one_gib_and_all_empty(cuda, oracle):
     for chained in (0, N.HS_KIND_FLAG_CHAINED):
         out = _call(L, torch, buf, b0, b1, N.HS_KIND_NAIVE | N.HS_KIND_FLAG_MERGE | chained, ws=ws)
         assert (out[0] == n // 256).all().item()
-        assert not ws.any().item()
+        assert ws_clean(ws)
     out = _call(L, torch, buf, b0, b0, N.HS_KIND_NAIVE | N.HS_KIND_FLAG_MERGE, ws=ws)
     assert (out[0] == 0).all().item()
 
@@ -201,7 +202,7 @@ def test_workspace_per_stream(cuda, oracle):
         want = oracle.histogram(hosts[j])
         for o in outs[j]:
             assert np.array_equal(o.cpu().numpy().view(np.uint64), want)
-        assert not st.workspace((s1, s2)[j]).any().item()
+        assert ws_clean(st.workspace((s1, s2)[j]))
 
 
 def test_lane_accepts_large_slot_totals(cuda, oracle):
