@@ -265,6 +265,11 @@ int hs_binning_pattern(const uint64_t* h_prior, int64_t total_slots, int64_t cap
 int hs_degeneracy(const uint64_t* h_counts, double* max_bin_fraction, int* argmax_bin,
                   uint64_t* total);
 
+/* divergence (policy.py:56-64): half the L1 distance of the two normalised histograms,
+ * summed in numpy's pairwise order, so the value is the reference's bit for bit.
+ * HS_ERR_INVALID_ARG when either histogram is empty (the reference's EmptyHistogram). */
+int hs_divergence(const uint64_t* h_a, const uint64_t* h_b, double* out);
+
 /* ---- seeded generators (datagen.py:92-155; splitmix64, byte-exact) ------ */
 #define HS_GEN_UNIFORM 0
 #define HS_GEN_SEQUENTIAL 1

@@ -129,6 +129,45 @@ int hs_degeneracy(const uint64_t* counts, double* frac, int* argmax, uint64_t* t
   return HS_OK;
 }
 
+// numpy's pairwise float64 sum (numpy 2.x pairwise_sum, PW_BLOCKSIZE 128): blocks of at
+// most 128 elements are summed with 8 interleaved accumulators combined as
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)); longer runs split at a multiple of 8 below n/2.
+static double pairwise_sum(const double* a, int n) {
+  if (n < 8) {
+    double r = 0.0;
+    for (int i = 0; i < n; ++i) r += a[i];
+    return r;
+  }
+  if (n <= 128) {
+    double r[8];
+    for (int j = 0; j < 8; ++j) r[j] = a[j];
+    int i = 8;
+    for (; i < n - (n % 8); i += 8)
+      for (int j = 0; j < 8; ++j) r[j] += a[i + j];
+    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    for (; i < n; ++i) res += a[i];
+    return res;
+  }
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  return pairwise_sum(a, n2) + pairwise_sum(a + n2, n - n2);
+}
+
+int hs_divergence(const uint64_t* a, const uint64_t* b, double* out) {
+  if (!a || !b || !out) return HS_ERR_INVALID_ARG;
+  uint64_t ta = 0, tb = 0;
+  for (int k = 0; k < 256; ++k) {
+    ta += a[k];
+    tb += b[k];
+  }
+  if (ta == 0 || tb == 0) return HS_ERR_INVALID_ARG;
+  const double da = double(ta), db = double(tb);
+  double d[256];
+  for (int k = 0; k < 256; ++k) d[k] = std::fabs(double(a[k]) / da - double(b[k]) / db);
+  *out = 0.5 * pairwise_sum(d, 256);
+  return HS_OK;
+}
+
 int hs_generate_host(int kind, uint64_t seed, int value, double mean, double sigma, double degeneracy,
                      uint8_t* out, uint64_t n, int threads) {
   if (n == 0) return HS_OK;

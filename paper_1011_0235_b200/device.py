@@ -117,7 +117,7 @@ class Staging:
 
     Reuse is safe once the work that read it has completed; the synchronous API
     waits for its readback, the pipeline releases a slot only after its batch is
-    folded (stream.py:_StageBuffer protocol)."""
+    folded (stream.py:_Slot protocol)."""
 
     def __init__(self, device=None):
         t = require_cuda()

@@ -150,6 +150,24 @@ def test_policy_matches_reference(golden):
             assert hs.divergence(a, b) == m["divergence"]
 
 
+def test_native_divergence_is_numpy_pairwise(oracle):
+    """hs_divergence (native, numpy's pairwise summation order) against the oracle's numpy
+    restatement of policy.py:56-64, bit for bit, over count scales from 1 to 2**62."""
+    rng = np.random.default_rng(64)
+    for trial in range(4000):
+        scale_a, scale_b = 2 ** int(rng.integers(1, 62)), 2 ** int(rng.integers(1, 62))
+        a = rng.integers(0, scale_a, 256, dtype=np.uint64)
+        b = rng.integers(0, scale_b, 256, dtype=np.uint64)
+        if trial % 5 == 0:
+            a[rng.random(256) < 0.9] = 0
+        if int(a.sum(dtype=object)) == 0 or int(b.sum(dtype=object)) == 0 or a.sum(dtype=object) >= 2**64:
+            continue
+        if b.sum(dtype=object) >= 2**64:
+            continue
+        want = oracle.divergence(a, b)
+        assert hs.divergence(hs.Histogram256(a), hs.Histogram256(b)) == want, trial
+
+
 def test_policy_edges():
     assert hs.degeneracy(hs.zero_histogram()) == hs.DegeneracyReport(0.0, 0, 0)
     assert hs.select_kernel(hs.DegeneracyReport(0.45, 5, 10), hs.SwitchPolicy(0.45)) is hs.KernelKind.ADAPTIVE

@@ -25,16 +25,16 @@ def wrap(mod, name, expect_us=None):
             return f(*a, **k)
         finally:
             d = (time.perf_counter() - t) * 1e3
-            extra = d - (a[0] / 1e3 if expect_us and a and isinstance(a[0], (int, float)) else 0)
+            extra = d - (a[0] / 1e3 if expect_us and a and isinstance(a[0], (int, float)) else 0)  # _nap(us)
             log.append((threading.current_thread().name, name, round((t - T0[0]) * 1e3, 2), round(d, 2),
                         round(extra, 2)))
     setattr(mod, name, g)
 
 
 wrap(S.D, "stage")
-wrap(S, "_launch_wait")
-wrap(S, "_fetch")
-wrap(S, "_sleep_us", expect_us=True)
+wrap(S._Counter, "wait_kernel")
+wrap(S._Counter, "collect")
+wrap(S, "_nap", expect_us=True)
 
 
 class Src:
@@ -63,5 +63,5 @@ for rep in range(12):
     tins = [round(s.transfer_in_ns / 1e6, 1) for s in r.stages]
     print(rep, "ratio %.4f" % r.pipelined_ratio, "tin", tins, flush=True)
     for row in log:
-        if row[4] > 3.0 or (row[1] != "_sleep_us" and row[3] > 3.0):
+        if row[4] > 3.0 or (row[1] != "_nap" and row[3] > 3.0):
             print("   slow:", row, flush=True)
