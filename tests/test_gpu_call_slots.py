@@ -2,7 +2,7 @@
 ticketed calls on one workspace count into rotating slots, so a call's CTAs flush while
 its predecessor is still draining and only the CTAs that store the output wait for it.
 
-Checked here, all against host bincounts and with the workspace clean afterwards:
+Checked here, all against the oracle's counts and with the workspace clean afterwards:
 - long unsynchronised sequences of random calls on one stream and one workspace --
   single and multi-segment, merged and per-segment, tiny (one CTA) to > 1 GiB
   (several chained launches per call), groups larger than the workspace's rows,
@@ -44,7 +44,9 @@ def stream_data(cuda):
 
 
 def _counts(host, a, b):
-    return np.bincount(host[a:b], minlength=256).astype(np.uint64)
+    from oracle import oracle as O
+
+    return O.histogram_mt(host[a:b]) if b - a > (64 << 20) else O.histogram(host[a:b])
 
 
 @pytest.mark.parametrize("seed", range(3))

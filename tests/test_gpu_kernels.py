@@ -401,10 +401,10 @@ def test_graph_replay_ticketed(cuda, oracle):
 
 
 @pytest.mark.parametrize("seed", range(4))
-def test_fuzz_segment_layouts(cuda, seed):
+def test_fuzz_segment_layouts(cuda, oracle, seed):
     """Random batches through the C ABI: 1-300 segments of random word-multiple sizes
     (empty ones included) at random word offsets of one buffer, every impl and kind,
-    with a workspace sized for 64 or 256 segments or none. Counts equal numpy's."""
+    with a workspace sized for 64 or 256 segments or none. Counts equal the oracle's."""
     torch = cuda
     rng = np.random.default_rng(1000 + seed)
     n = 48 << 20
@@ -421,7 +421,7 @@ def test_fuzz_segment_layouts(cuda, seed):
         starts = 4 * rng.integers(0, (n - int(sizes.max()) - 4) // 4, nseg)
         b0 = starts.astype(np.uint64)
         b1 = (starts + sizes).astype(np.uint64)
-        want = np.stack([np.bincount(host[a:b], minlength=256) for a, b in zip(b0, b1)]).astype(np.uint64)
+        want = np.stack([oracle.histogram(host[a:b]) for a, b in zip(b0, b1)])
         impl = int(rng.choice([N.HS_IMPL_AUTO, N.HS_IMPL_LANE, N.HS_IMPL_WARP]))
         kind = int(rng.choice([N.HS_KIND_NAIVE, N.HS_KIND_ADAPTIVE]))
         ws_seg = int(rng.choice([0, 64, 256]))
