@@ -68,15 +68,21 @@ class _PinnedRegistry:
         self._starts: list[int] = []
         self._ends: list[int] = []
 
-    def add(self, tensor) -> None:
-        start = tensor.data_ptr()
-        end = start + tensor.numel() * tensor.element_size()
+    def add(self, arr: np.ndarray) -> None:
+        start = arr.ctypes.data
+        end = start + arr.nbytes
         with self._lock:
             i = bisect.bisect_left(self._starts, start)
             self._starts.insert(i, start)
             self._ends.insert(i, end)
-        # the numpy view keeps the tensor alive; the range is dropped with it
-        weakref.finalize(tensor, self._drop, start)
+        # The range lives as long as the memory: tie it to the object at the end of the
+        # array's base chain, which every numpy view of it keeps alive (not to the torch
+        # tensor that allocated it: tensor.numpy() holds another alias of the storage,
+        # and the original tensor object can die while the memory is still in use).
+        owner = arr
+        while isinstance(owner, np.ndarray) and owner.base is not None:
+            owner = owner.base
+        weakref.finalize(owner, self._drop, start)
 
     def _drop(self, start: int) -> None:
         with self._lock:
@@ -97,9 +103,9 @@ _pinned = _PinnedRegistry()
 def pinned_bytes(n: int) -> np.ndarray:
     """A uint8 numpy array backed by page-locked host memory (async H2D source)."""
     t = require_cuda().empty(max(int(n), 1), dtype=torch().uint8, pin_memory=True)
-    _pinned.add(t)
-    arr = t.numpy()[: int(n)]
-    return arr
+    full = t.numpy()
+    _pinned.add(full)
+    return full[: int(n)]
 
 
 def pinned_words(n_words: int) -> np.ndarray:
@@ -123,6 +129,7 @@ class Staging:
         t = require_cuda()
         self.device = t.device("cuda", t.cuda.current_device() if device is None else t.device(device).index)
         self._dev = None
+        self._bounce = None
         self._out_host = None
         self._out_dev = None
         self._ws: dict[int, object] = {}  # stream handle -> workspace (insertion = LRU order)
@@ -136,6 +143,15 @@ class Staging:
             self._dev = t.empty(cap + 256, dtype=t.uint8, device=self.device)
         # 256-B aligned start (the allocator returns 512-B aligned blocks)
         return self._dev
+
+    def host_bounce(self, n: int) -> np.ndarray:
+        """Page-locked bounce buffer for pageable host chunks: they are copied here on
+        the host and DMA'd from here, so the H2D stays asynchronous and never goes
+        through the driver's pageable-copy path (which serialises with other threads'
+        CUDA calls: 20-110 ms stalls in run_pipeline, tools/diag/c07_probe.py)."""
+        if self._bounce is None or self._bounce.size < n:
+            self._bounce = pinned_bytes(max(int(n), 1 << 20))
+        return self._bounce
 
     _MAX_WS = 32
 
@@ -288,6 +304,7 @@ def stage(chunks: Sequence, staging: Staging | None, stream=None) -> StagedBatch
         # chunks that sit back to back in host memory (slices of one pinned stream) go
         # in one copy: 16 MiB copies reach 54.5 GB/s, 128 MiB ones 55.2 GB/s
         runs: list[list] = []  # [host_ptr, dev_off, nbytes, first chunk array]
+        bounce = None  # pageable chunks go through the staging's pinned bounce buffer
         for i, c in host:
             n = c.byte_size
             ptrs[i] = base + off
@@ -306,6 +323,11 @@ def stage(chunks: Sequence, staging: Staging | None, stream=None) -> StagedBatch
                     arr = first.view(np.uint8)
                 else:  # the run spans several chunks' memory (all kept alive above)
                     arr = np.ctypeslib.as_array((ctypes.c_uint8 * n).from_address(hp))
+                if not _pinned.contains(hp, n):
+                    if bounce is None:
+                        bounce = staging.host_bounce(total)
+                    np.copyto(bounce[doff:doff + n], arr)
+                    arr = bounce[doff:doff + n]
                 with warnings.catch_warnings():  # chunks are read-only views; torch only reads them
                     warnings.simplefilter("ignore", UserWarning)
                     src = t.from_numpy(arr)
@@ -555,8 +577,9 @@ def group_slots(chunk, pattern, group_size: int, group_count: int, mode: int) ->
 def ablation_stage(chunk, stage_id: int, pattern, repeats: int | None = None):
     """One genealogy stage (hs_ablation_stage): ``repeats`` back-to-back launches over
     the chunk between two CUDA events on the launch stream (default: enough to stream
-    >= 256 MiB, 3..20 launches), so a stage is timed as a streaming kernel rather than as
-    one isolated launch's latency. Returns (seconds per launch, device sink of the last
+    >= 1 GiB, 8..32 launches, all queued before the first runs), so a stage is timed as a
+    streaming kernel rather than as one isolated launch's latency or the host's issue
+    rate. Returns (seconds per launch, device sink of the last
     launch, histogram-or-None)."""
     t = require_cuda()
     stream = t.cuda.current_stream()
@@ -568,8 +591,8 @@ def ablation_stage(chunk, stage_id: int, pattern, repeats: int | None = None):
     off_p, cnt_p, S, cap, keep = _pattern_args(pattern)
     base = staged.base + int(staged.begin[0]) if staged.nbytes else 0
     n = staged.nbytes
-    if repeats is None:
-        repeats = int(min(20, max(3, -(-(256 << 20) // max(n, 1)))))
+    if repeats is None:  # >= 1 GiB streamed per sample, 8..32 launches
+        repeats = int(min(32, max(8, -(-(1 << 30) // max(n, 1)))))
     L = N.lib()
 
     def once():
@@ -579,6 +602,11 @@ def ablation_stage(chunk, stage_id: int, pattern, repeats: int | None = None):
     once()  # first-launch costs (module load, smem attribute) outside the timing
     a = t.cuda.Event(enable_timing=True)
     b = t.cuda.Event(enable_timing=True)
+    # hold the stream (~2 ms) while the host queues every launch, so the events time the
+    # launches back to back on the device, not the host's issue rate (a 64 MiB stage
+    # launch is ~15 us of device time, about what one Python-issued call takes)
+    with t.cuda.stream(stream):
+        t.cuda._sleep(4_000_000)
     a.record(stream)
     for _ in range(repeats):
         once()

@@ -49,3 +49,74 @@ def pytest_collection_modifyitems(config, items):
         for suffix, reason in TIMING_XFAIL.items():
             if item.nodeid.endswith(suffix):
                 item.add_marker(pytest.mark.xfail(reason=reason, strict=False))
+
+
+# Diagnostics (off unless HS_PIPELINE_TRACE names a file): time every step of both
+# run_pipeline threads and append the steps that ran > 3 ms past their synthetic delay,
+# with the run's ratio, to that file -- to find what stalls a timing criterion.
+if os.environ.get("HS_PIPELINE_TRACE"):
+    import threading as _th
+    import time as _time
+
+    from paper_1011_0235_b200 import device as _D
+    from paper_1011_0235_b200 import stream as _S
+
+    _log: list = []
+
+    def _wrap(owner, name, delay_arg=False):
+        f = getattr(owner, name)
+
+        def g(*a, **k):
+            t0 = _time.perf_counter_ns()
+            try:
+                return f(*a, **k)
+            finally:
+                d = (_time.perf_counter_ns() - t0) / 1e6
+                want = (a[0] / 1e3) if delay_arg and a and isinstance(a[0], (int, float)) else 0.0
+                if d - want > 3.0:
+                    _log.append((_th.current_thread().name, name, round(d, 2), round(want, 2)))
+
+        setattr(owner, name, g)
+
+    for _o, _n, _d in ((_S, "_nap", True), (_S, "_draw", False), (_D, "stage", False), (_S._Slot, "take", False),
+                       (_S._Counter, "issue", False), (_S._Counter, "wait_kernel", False),
+                       (_S._Counter, "collect", False), (_S._Fold, "decide", False), (_S._Fold, "absorb", False)):
+        _wrap(_o, _n, _d)
+    import gc as _gc
+
+    import torch as _torch
+
+    from paper_1011_0235_b200 import _native as _N
+
+    for _o, _n in ((_torch.Tensor, "copy_"), (_torch, "empty"), (_torch.cuda.Event, "record"),
+                   (_torch.cuda.Event, "synchronize"), (_torch, "from_numpy")):
+        _wrap(_o, _n)
+    _L = _N.lib()
+    _wrap(_L, "hs_histogram_batched")
+    _gc_t0 = {}
+
+    def _gc_cb(phase, info):
+        if phase == "start":
+            _gc_t0[info["generation"]] = _time.perf_counter_ns()
+        else:
+            d = (_time.perf_counter_ns() - _gc_t0.get(info["generation"], _time.perf_counter_ns())) / 1e6
+            if d > 3.0:
+                _log.append((_th.current_thread().name, f"gc{info['generation']}", round(d, 2), 0.0))
+
+    _gc.callbacks.append(_gc_cb)
+    _run = _S.run_pipeline
+
+    def _traced(*a, **k):
+        _log.clear()
+        res = _run(*a, **k)
+        with open(os.environ["HS_PIPELINE_TRACE"], "a") as fh:
+            fh.write(f"run n={a[1].num_iterations} ratio={res[2].pipelined_ratio:.4f} slow={_log}\n")
+        return res
+
+    _S.run_pipeline = _traced
+    histostream.run_pipeline = _traced
+    import sys as _sys
+
+    for _m in list(_sys.modules.values()):
+        if getattr(_m, "run_pipeline", None) is _run:
+            _m.run_pipeline = _traced

@@ -226,3 +226,33 @@ def test_device_stream_batched_fold(cuda, window, batch):
     assert states_equal(seq, dev)
     assert [k.value for k in seq[3]] == [k.value for k in dev[3]]
     assert np.array_equal(np.stack([h.counts for h in seq[1].ring]), np.stack([h.counts for h in dev[1].ring]))
+
+
+def test_pinned_chunks_dma_directly_pageable_through_bounce(cuda, oracle):
+    """Staging keeps page-locked chunks on the direct DMA path for as long as any view of
+    them lives (the registry follows the memory, not the tensor that allocated it), and
+    copies pageable chunks through the staging's pinned bounce buffer; counts exact."""
+    import gc
+
+    torch = cuda
+    from paper_1011_0235_b200 import device as D
+
+    arr = D.pinned_bytes(1 << 20)
+    arr[:] = oracle.generate("normal", 1 << 20, 5, mean=90.0, sigma=20.0)
+    words = arr.view(np.uint32)[16:]
+    want = oracle.histogram(arr[64:64 + 4096])
+    del arr
+    gc.collect()
+    assert D.is_pinned(words)
+    st = D.Staging()
+    stream = torch.cuda.current_stream()
+    staged = D.stage([hs.PackedChunk(words[:1024])], st, stream)
+    assert st._bounce is None  # direct DMA
+    out = D.launch(staged, 0, None, stream, staging=st)  # HS_KIND_NAIVE
+    assert np.array_equal(out.cpu().numpy().view(np.uint64)[0], want)
+    page = np.ascontiguousarray(words[:1024]).copy()
+    assert not D.is_pinned(page)
+    staged = D.stage([hs.PackedChunk(page)], st, stream)
+    assert st._bounce is not None
+    out = D.launch(staged, 0, None, stream, staging=st)
+    assert np.array_equal(out.cpu().numpy().view(np.uint64)[0], want)
