@@ -3,8 +3,9 @@
 multiples), overlapping offsets, every impl and kind, hot-bin hints, workspaces for
 64/256/1000 segments or none, and the blocking entry with page-locked and pageable
 result buffers; round 2: merged outputs (HS_KIND_FLAG_MERGE: one row = the sum of
-the segments) and chained calls (HS_KIND_FLAG_CHAINED). Runs for SECONDS; prints one
-line per trial class and a summary.
+the segments), chained calls (HS_KIND_FLAG_CHAINED) and bursts of 8-40 calls issued back
+to back on one workspace with no synchronisation in between (the rotating call slots).
+Runs for SECONDS; prints a progress line every 25 trials and a summary.
 usage: python tools/fuzz_long.py [SECONDS]"""
 import os
 import sys
@@ -38,7 +39,60 @@ wss = {k: torch.zeros(int(L.hs_workspace_bytes(k)), dtype=torch.uint8, device="c
 pinned = torch.empty(600 * 256, dtype=torch.int64).pin_memory()
 trials = bytes_total = 0
 t_end = time.time() + secs
+HEAD = 384  # include/hist256.h HS_WS_HEAD_BYTES: the slots after it are zero between calls
+
+
+def slots_clean(ws) -> bool:
+    return not ws[HEAD:].any().item()
+
+
+def burst() -> int:
+    """8-40 calls back to back on one workspace (small ones rotate through the call
+    slots, large ones use the serial slot), then every output checked."""
+    ws = wss[int(rng.choice([64, 256, 1000]))]
+    calls = []
+    for _ in range(int(rng.integers(8, 41))):
+        nseg = int(rng.choice([1, 1, 1, 2, 7, 64]))
+        sizes = (rng.choice([4, 4096, 1 << 20, 4 << 20, 16 << 20, 40 << 20], size=nseg)
+                 + 4 * rng.integers(0, 1 << 12, nseg)).astype(np.int64)
+        if rng.random() < 0.05:
+            sizes[0] = 4 * rng.integers(1 << 28, 5 << 27)
+        starts = 4 * rng.integers(0, (n - sizes) // 4)
+        b0, b1 = starts.astype(np.uint64), (starts + sizes).astype(np.uint64)
+        kind = int(rng.choice([N.HS_KIND_NAIVE, N.HS_KIND_ADAPTIVE]))
+        if rng.random() < 0.6:
+            kind |= N.HS_KIND_FLAG_CHAINED
+        merge = rng.random() < 0.3
+        if merge:
+            kind |= N.HS_KIND_FLAG_MERGE
+        pat = pats[rng.integers(0, 4)]
+        out = torch.full((nseg, 256), -1, dtype=torch.int64, device="cuda")
+        N.check(L.hs_histogram_batched(buf.data_ptr(), N.u64p(b0), N.u64p(b1), nseg, kind, N.HS_IMPL_AUTO,
+                                       N.i64p(pat.offset), N.i64p(pat.count), 960, 8, out.data_ptr(),
+                                       ws.data_ptr(), ws.numel(), st), "burst")
+        calls.append((b0, b1, merge, out))
+    total = 0
+    for k, (b0, b1, merge, out) in enumerate(calls):
+        want = np.stack([torch.bincount(buf[int(a):int(b)], minlength=256).cpu().numpy().astype(np.uint64)
+                         for a, b in zip(b0, b1)])
+        got = out.cpu().numpy().view(np.uint64)
+        if merge:
+            got, want = got[:1], want.sum(axis=0, dtype=np.uint64)[None, :]
+        if not np.array_equal(got, want):
+            print(f"MISMATCH burst call {k}: nseg {b0.size} merge {merge}", flush=True)
+            raise SystemExit(1)
+        total += int((b1 - b0).sum())
+    if not slots_clean(ws):
+        print("MISMATCH burst: workspace slots not left zero", flush=True)
+        raise SystemExit(1)
+    return total
+
+
 while time.time() < t_end:
+    if rng.random() < 0.3:
+        bytes_total += burst()
+        trials += 1
+        continue
     nseg = int(rng.choice([1, 3, 64, 65, 255, 256, 257, 511, 600]))
     big = rng.random() < 0.15
     scale = [0, 4, 4096, 1 << 20, 16 << 20] + ([1 << 30, (5 << 29)] if big else [])
@@ -83,7 +137,7 @@ while time.time() < t_end:
         got, want = got[:1], want.sum(axis=0, dtype=np.uint64)[None, :]
     ok = np.array_equal(got, want)
     if ws is not None:
-        ok = ok and not ws.any().item()
+        ok = ok and slots_clean(ws)
     trials += 1
     bytes_total += int(sizes.sum())
     if not ok:
