@@ -296,6 +296,43 @@ def cpu_reference_run(seconds: float, chunks_per_step: int | None = None, steps:
             "step_seconds": times}
 
 
+def cpu_reference_paths(seconds: float):
+    """The reference's other two CPU entry points on the same 16 MiB C5 chunks (SURVEY
+    §8(d)): the serial oracle reference_histogram (kernels.py:330-333) and
+    adaptive_histogram (kernels.py:349-384, pattern from the previous chunk's histogram,
+    WorkerGroupConfig(32, cores)), each for about ``seconds`` and checked against the
+    oracle. Returns {name: {value GB/s, chunks}} or None without baseline/_ref."""
+    K = _ref_module()
+    if K is None:
+        return None
+    from histostream.core import PackedChunk as RefChunk
+    from histostream.pattern import compute_binning_pattern
+    from oracle import oracle as O
+
+    cores = host_cores()
+    cfg = K.WorkerGroupConfig(32, cores)
+    pool = c5_sample_words(4)
+    chunks = [RefChunk(w) for w in pool]
+    pattern = compute_binning_pattern(K.reference_histogram(chunks[-1]))
+    runs = {"reference_histogram": lambda c: K.reference_histogram(c),
+            "adaptive_histogram": lambda c: K.adaptive_histogram(c, pattern, cfg)}
+    out = {}
+    for name, fn in runs.items():
+        fn(chunks[0])  # JIT / first touch
+        done, t0 = 0, time.perf_counter()
+        while True:
+            h = fn(chunks[done % len(chunks)])
+            if done < len(chunks):
+                assert np.array_equal(np.asarray(h.counts), O.histogram(pool[done].view(np.uint8))), name
+            done += 1
+            if time.perf_counter() - t0 >= seconds:
+                break
+        dt = time.perf_counter() - t0
+        out[name] = {"value": round(done * CHUNK / dt / 1e9, 4), "unit": "GB/s", "chunks": done,
+                     "cores": 1 if name == "reference_histogram" else cores}
+    return out
+
+
 def cpu_port_run(seconds: float):
     """The oracle's C restatement of the reference's naive worker (kernels.py:97-130,
     arbitration loop), one group thread per host core, on the same sample."""
@@ -509,6 +546,9 @@ def main(argv=None):
         if ref is not None:
             ref.pop("step_seconds", None)
             cpu = dict(ref, port=port)
+            others = cpu_reference_paths(max(2.0, args.cpu_seconds / 3))
+            if others:
+                cpu["other_reference_paths"] = others
         else:
             cpu = port
 
