@@ -472,11 +472,13 @@ __device__ __forceinline__ void lane_flush(uint32_t sbase, unsigned long long* _
 // The rotating call's last finalization releases its slot
 __device__ __forceinline__ void release_slot(const Tickets& tk, const SlotView& sv, int m) {
   if (threadIdx.x != 0) return;
+  // (the caller's barrier orders the CTA's drains before thread 0; the fence makes the
+  // release cover them at GPU scope)
+  __threadfence();
   if (unsigned(m) == tk.nfinal) {  // the call's only finalizing CTA
     st_release_u32(&tk.hdr->drained[sv.slot], sv.epoch + 1);
     return;
   }
-  __threadfence();
   if (atomicAdd(&tk.hdr->finalized[sv.slot], unsigned(m)) + unsigned(m) == tk.nfinal) {
     tk.hdr->finalized[sv.slot] = 0;
     __threadfence();
