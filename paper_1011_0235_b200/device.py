@@ -130,6 +130,7 @@ class Staging:
         self.device = t.device("cuda", t.cuda.current_device() if device is None else t.device(device).index)
         self._dev = None
         self._bounce = None
+        self._bounce_done = None  # event after the last copies out of the bounce buffer
         self._out_host = None
         self._out_dev = None
         self._ws: dict[int, object] = {}  # stream handle -> workspace (insertion = LRU order)
@@ -326,6 +327,8 @@ def stage(chunks: Sequence, staging: Staging | None, stream=None) -> StagedBatch
                 if not _pinned.contains(hp, n):
                     if bounce is None:
                         bounce = staging.host_bounce(total)
+                        if staging._bounce_done is not None:  # its previous DMA must have read it
+                            staging._bounce_done.synchronize()
                     np.copyto(bounce[doff:doff + n], arr)
                     arr = bounce[doff:doff + n]
                 with warnings.catch_warnings():  # chunks are read-only views; torch only reads them
@@ -335,6 +338,8 @@ def stage(chunks: Sequence, staging: Staging | None, stream=None) -> StagedBatch
                 keep.append(src)
             ready = t.cuda.Event()
             ready.record(stream)
+            if bounce is not None:
+                staging._bounce_done = ready
     for i, c in enumerate(chunks):
         if isinstance(c, DeviceChunk):
             ptrs[i] = c.data.data_ptr()
