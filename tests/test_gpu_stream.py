@@ -256,3 +256,25 @@ def test_pinned_chunks_dma_directly_pageable_through_bounce(cuda, oracle):
     assert st._bounce is not None
     out = D.launch(staged, 0, None, stream, staging=st)
     assert np.array_equal(out.cpu().numpy().view(np.uint64)[0], want)
+
+
+def test_pageable_batches_back_to_back_on_one_staging(cuda, oracle):
+    """Two pageable batches staged on one Staging with no synchronisation in between: the
+    second waits for the first's DMA out of the bounce buffer before refilling it."""
+    torch = cuda
+    from paper_1011_0235_b200 import device as D
+
+    st = D.Staging()
+    stream = torch.cuda.current_stream()
+    a = oracle.generate("normal", 8 << 20, 11, mean=60.0, sigma=10.0)
+    b = oracle.generate("normal", 8 << 20, 12, mean=190.0, sigma=10.0)
+    s1 = D.stage([hs.PackedChunk(a.view(np.uint32))], st, stream)
+    out1 = D.launch(s1, 0, None, stream, staging=st).clone()
+    st2 = D.Staging()  # a second device buffer, the same bounce-buffer discipline
+    s2 = D.stage([hs.PackedChunk(b.view(np.uint32))], st2, stream)
+    out2 = D.launch(s2, 0, None, stream, staging=st2)
+    s3 = D.stage([hs.PackedChunk(b.view(np.uint32))], st, stream)  # refills st's bounce buffer
+    out3 = D.launch(s3, 0, None, stream, staging=st)
+    assert np.array_equal(out1.cpu().numpy().view(np.uint64)[0], oracle.histogram(a))
+    assert np.array_equal(out2.cpu().numpy().view(np.uint64)[0], oracle.histogram(b))
+    assert np.array_equal(out3.cpu().numpy().view(np.uint64)[0], oracle.histogram(b))
