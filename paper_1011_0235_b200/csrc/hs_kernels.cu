@@ -1909,8 +1909,10 @@ int histogram_batched(const uint8_t* d_data, const uint64_t* h_begin, const uint
     if (reinterpret_cast<uintptr_t>(d_ws) & 15) return HS_ERR_ALIGNMENT;
     tk = tickets_of(d_ws, ws_bytes, group);
     if (merge) group = kMaxSeg;  // one accumulator row whatever the segment count
-    // a merged call over several groups finalizes once, in its last group: serial
-    if (merge && nseg <= group) plan_call(tk, h_begin, h_end, 0, nseg, true);
+    // a merged call over several groups finalizes once, in its last group: serial. So
+    // are the blocking entries (latency): the host waits for each call, so there is no
+    // next call to overlap and the arrival would only add its round trip.
+    if (merge && nseg <= group && !latency) plan_call(tk, h_begin, h_end, 0, nseg, true);
   } else {
     cudaError_t e = cudaMemsetAsync(d_out, 0, size_t(merge ? 1 : nseg) * 256 * sizeof(uint64_t), st);
     if (e != cudaSuccess) return fold(e);
@@ -1932,7 +1934,7 @@ int histogram_batched(const uint8_t* d_data, const uint64_t* h_begin, const uint
       if (e != cudaSuccess) return fold(e);
       continue;
     }
-    if (!merge) plan_call(tk, h_begin, h_end, s0, ns, false);  // each group is a call of its own
+    if (!merge && !latency) plan_call(tk, h_begin, h_end, s0, ns, false);  // each group is a call of its own
     rc = launch_segments(d_data, h_begin, h_end, s0, ns, kind, impl, have_pattern ? &pp : nullptr,
                          reinterpret_cast<unsigned long long*>(d_out), st, di, tk, 0, latency, wait_first, merge,
                          last_busy < s0 + ns);
