@@ -2180,6 +2180,7 @@ int hs_stream_step(const uint8_t* d_data, const uint64_t* h_begin, const uint64_
   int rows = 0;
   Tickets tk = tickets_of(d_ws, ws_bytes, rows);
   plan_call(tk, h_begin, h_end, 0, nseg, false);
+  tk.rotate = tk.nfinal > 0 && total <= kLaunchBytes;  // followed by the fold, as hs_stream_block
   bool empty = total == 0;
   if (empty) {
     cudaError_t e = cudaMemsetAsync(d_out, 0, size_t(nseg) * 256 * sizeof(uint64_t), st);
