@@ -25,8 +25,10 @@
 //     dominated by one value it counts that hot bin's all-hot 16-byte vectors in a
 //     register (no shared-memory traffic at all on degenerate input).
 //   * Launches are chained with programmatic dependent launch (griddepcontrol): a launch
-//     streams while the previous one's tail drains and waits only before its first
-//     global write. Output is ticketed: one kernel per launch, no memset.
+//     streams while the previous one's tail drains. Output is ticketed (one kernel per
+//     launch, no memset) through a workspace slot: large calls use the serial slot and
+//     wait for their predecessor before their first RED; small single-launch calls take
+//     rotating slots, so only their output store waits (WsHeader).
 //   * CTA ranges are whole 4 KiB units of the launch's concatenated range; full-grid
 //     launches over several segments weight the split so that a CTA crossing a segment
 //     boundary (and paying a flush there) gets less data.
