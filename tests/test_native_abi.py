@@ -187,3 +187,18 @@ def _build_c_demo(tmp_path):
 def test_c_demo_compiles_against_the_header(tmp_path):
     """The ABI is usable from plain C: the demo builds with -Wall -Wextra -Werror."""
     assert _build_c_demo(tmp_path).exists()
+
+
+def test_workspace_layout_matches_header():
+    """hs_workspace_bytes(n) = HS_WS_HEAD_BYTES + (HS_WS_SLOTS + 1) call slots of 1 KiB of
+    tickets + one 2 KiB accumulator row per segment (n clamped to [64, 256]); the stream
+    block workspace embeds the 256-row form."""
+    hdr = HEADER.read_text()
+    head = int(re.search(r"#define HS_WS_HEAD_BYTES (\d+)", hdr).group(1))
+    slots = int(re.search(r"#define HS_WS_SLOTS (\d+)", hdr).group(1))
+    lib = N.lib()
+    for n, rows in ((1, 64), (64, 64), (100, 100), (256, 256), (1000, 256)):
+        assert lib.hs_workspace_bytes(n) == head + (slots + 1) * (1024 + rows * 2048), n
+    assert lib.hs_workspace_bytes(-1) == 0
+    assert head % 16 == 0 and head >= 8 + 2 * 4 * slots
+    assert lib.hs_stream_block_ws_bytes(4, 8) > lib.hs_workspace_bytes(256)
