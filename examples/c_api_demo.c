@@ -65,7 +65,7 @@ int main(void) {
   cuda_check(cudaMalloc((void**)&d, n), "cudaMalloc data");
   cuda_check(cudaMalloc((void**)&d_out, sizeof(got)), "cudaMalloc out");
   cuda_check(cudaMalloc(&d_ws, ws), "cudaMalloc workspace");
-  cuda_check(cudaMemset(d_ws, 0, ws), "zero workspace");  /* once; every call leaves it zero */
+  cuda_check(cudaMemset(d_ws, 0, ws), "zero workspace");  /* once; calls leave its slots zero */
   cuda_check(cudaMemcpy(d, h, n, cudaMemcpyHostToDevice), "H2D");
 
   /* 2. NAIVE over three segments: one launch, counts written by the last CTA of each */

@@ -159,7 +159,7 @@ class Staging:
     def workspace(self, stream=None):
         """Device workspace of hs_histogram_batched (per-segment tickets + partials) for
         launches on ``stream`` (a torch stream, a raw handle, or None for the current
-        stream), zeroed once; every launch leaves it zero again. Launches that share a
+        stream), zeroed once; every call leaves its slots zero again. Launches that share a
         workspace must be stream-ordered, so there is one per CUDA stream: two calls on
         unsynchronized streams never share accumulator rows. Each is allocated and
         zeroed on its own stream, so the caching allocator only ever hands its memory
