@@ -1654,7 +1654,16 @@ void split_grid(SegParams& sp, int grid, uint32_t split_cost = 0) {
 // so there the grid is sized for latency instead: >= 16 KiB per CTA below 48 MiB. On a
 // 1024x1024 image that is 64 CTAs instead of 4: 28 -> 18 us per blocking call, while
 // graph-replayed back-to-back launches lose 3% (tools/c1_breakdown.py).
+// Back-to-back small calls (rotating call slots) run faster on more, shorter CTAs: per
+// call, 1 MiB with 4 CTAs 2.38 us, 8 CTAs 2.03, 32 CTAs 1.85; 2 MiB 2.42 -> 2.0 us with
+// 32 CTAs; from 6 MiB on 256 KiB per CTA stays best (8 MiB with 64 CTAs: 2.95 -> 3.46 us;
+// tools/diag/late_wait_ab.py, profiles/r2_call_slots.txt). So <= 1 / 2 / 4 MiB calls get
+// 32 / 64 / 128 KiB per CTA.
 uint64_t lane_grid_for(uint64_t v, bool latency = false) {
+  if (!latency && v <= (4ull << 20)) {
+    const int s = v <= (1ull << 20) ? 15 : v <= (2ull << 20) ? 16 : 17;
+    return std::max<uint64_t>(1, (v + (1ull << s) - 1) >> s);
+  }
   const int shift = latency ? 14 : 18;
   if (v <= (48ull << 20)) return std::max<uint64_t>(1, std::min<uint64_t>(64, (v + (1ull << shift) - 1) >> shift));
   if (v <= (384ull << 20)) return 128;

@@ -25,8 +25,11 @@ out = torch.zeros((reps, 256), dtype=torch.int64, device="cuda")
 s = torch.cuda.current_stream()
 torch.cuda.synchronize()
 row = []
-for mib in (1, 4, 8, 16, 24, 32, 48, 64, 256):
-    size = mib << 20
+SIZES_KIB = [int(x) for x in os.environ.get("AB_KIB", "").split(",") if x] or \
+    [m << 10 for m in (1, 4, 8, 16, 24, 32, 48, 64, 256)]
+for kib in SIZES_KIB:
+    size = kib << 10
+    mib = kib / 1024
     b0, b1 = np.zeros(1, np.uint64), np.full(1, size, np.uint64)
     best = 1e9
     for rep in range(3):
@@ -43,7 +46,7 @@ for mib in (1, 4, 8, 16, 24, 32, 48, 64, 256):
         z.synchronize()
         best = min(best, a.elapsed_time(z) / reps * 1e3)
     if os.environ.get("AB_NOCHECK"):
-        row.append(f"{mib} MiB {best:.2f} us ({size / best / 1e3:.0f} GB/s)")
+        row.append(f"{mib:g} MiB {best:.2f} us ({size / best / 1e3:.0f} GB/s)")
         continue
     sums = out.sum(dim=1).cpu().numpy()
     assert (sums == size).all(), (mib, sums[:8])
@@ -51,5 +54,5 @@ for mib in (1, 4, 8, 16, 24, 32, 48, 64, 256):
                         for k in range(0, reps, 13)])
     assert torch.equal(want, out[0:reps:13]), "bins differ"
     assert all(not ws[k * wsb + 384:(k + 1) * wsb].any().item() for k in range(K)), "workspace slots not left zero"
-    row.append(f"{mib} MiB {best:.2f} us ({size / best / 1e3:.0f} GB/s)")
+    row.append(f"{mib:g} MiB {best:.2f} us ({size / best / 1e3:.0f} GB/s)")
 print(os.environ.get("HS_LIBHIST256", "shipped"), f"K={K}", " | ".join(row), flush=True)
