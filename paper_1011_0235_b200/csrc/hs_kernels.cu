@@ -1664,7 +1664,9 @@ uint64_t lane_grid_for(uint64_t v, bool latency = false) {
     const int s = v <= (1ull << 20) ? 15 : v <= (2ull << 20) ? 16 : 17;
     return std::max<uint64_t>(1, (v + (1ull << s) - 1) >> s);
   }
-  const int shift = latency ? 14 : 18;
+  // above 8 MiB, 512 KiB per CTA (up to 64): 10 MiB 3.52 -> 3.31 us, 12 MiB 3.89 -> 3.62,
+  // 24 MiB 5.89 -> 5.72; 16 and 32-48 MiB unchanged
+  const int shift = latency ? 14 : (v > (8ull << 20) ? 19 : 18);
   if (v <= (48ull << 20)) return std::max<uint64_t>(1, std::min<uint64_t>(64, (v + (1ull << shift) - 1) >> shift));
   if (v <= (384ull << 20)) return 128;
   return ~0ull;  // every resident slot
@@ -1678,7 +1680,15 @@ int launch_batch(const uint8_t* d_data, SegParams& sp, int kind, int impl, const
   if (v == 0) return HS_OK;
   cudaError_t e = cudaSuccess;
   if (impl == HS_IMPL_LANE) {
-    const uint64_t want = lane_grid_for(v, latency);
+    // A call that waits for its predecessor before loading cannot overlap it, so its
+    // grid is sized for its own latency: >= 64 KiB per CTA but at least min(64, v/16 KiB)
+    // CTAs, up to every resident slot. Back-to-back waiting calls (profiles/
+    // r2_call_slots.txt): 1 MiB 11.8 -> 8.5 us, 16 MiB 19.1 (32 CTAs) -> 12.4 us (256),
+    // 48 MiB 23.0 -> 15.3, 256 MiB 51.1 -> 46.3 us against the throughput grid.
+    const uint64_t want =
+        (wait_first && !latency && v <= (384ull << 20))
+            ? std::max<uint64_t>((v + (1ull << 16) - 1) >> 16, std::min<uint64_t>(64, (v + (1ull << 14) - 1) >> 14))
+            : lane_grid_for(v, latency);
     // reserve_slots CTA slots are left free (the device stream engine's fold CTA takes
     // one while the next histogram streams, instead of delaying one of its CTAs)
     const bool hot = kind == HS_KIND_ADAPTIVE && pp != nullptr && pp->hot_unique;

@@ -18,6 +18,8 @@ tot = 2 << 30
 buf = torch.empty(tot, dtype=torch.uint8, device="cuda")
 hs.generate_device(hs.SourceSpec("uniform", tot, 5), buf)
 K = int(os.environ.get("HS_AB_SLOTS", "8"))
+# AB_WAIT=1: plain calls (each waits for its predecessor before loading) instead of chained ones
+KIND = N.HS_KIND_NAIVE | (0 if os.environ.get("AB_WAIT") else N.HS_KIND_FLAG_CHAINED)
 wsb = int(L.hs_workspace_bytes(64))
 ws = torch.zeros(K * wsb, dtype=torch.uint8, device="cuda")
 reps = 64
@@ -39,7 +41,7 @@ for kib in SIZES_KIB:
         for k in range(reps):
             off = (k * size) % (tot - size)
             N.check(L.hs_histogram_batched(buf.data_ptr() + off, N.u64p(b0), N.u64p(b1), 1,
-                                           N.HS_KIND_NAIVE | N.HS_KIND_FLAG_CHAINED, 0, None, None, 0, 0,
+                                           KIND, 0, None, None, 0, 0,
                                            out[k].data_ptr(), ws.data_ptr() + (k % K) * wsb, wsb,
                                            s.cuda_stream), "x")
         z.record()
