@@ -563,6 +563,7 @@ def main(argv=None):
         extra["c3_switch_stream"] = X.c3_switch(hs, torch, dev)
         if pinned is not None:
             extra["c4_host_streamed_mixed"] = X.c4_mixed(hs, torch, dev, pinned)
+            extra["host_small_chunks_reference_default"] = X.host_small_chunks(hs, torch, dev, pinned)
     del pinned
 
     if rank == 0:

@@ -327,3 +327,31 @@ def c4_mixed(hs, torch, dev, pinned, steps: int = 2):
             "kernel_switches": sum(1 for a, b in zip(kinds, kinds[1:]) if a != b),
             "adaptive_iterations": kinds.count("adaptive"), "iterations": len(kinds),
             "parity": "accumulator == oracle multithreaded count of the 16 GiB, bin for bin"}
+
+
+def host_small_chunks(hs, torch, dev, pinned, n: int = 2048):
+    """The reference's default pipeline shape (1 MiB chunks, batch 1, window 128) streamed
+    from pinned host memory (the first 2 GiB of the e2e leg's buffer): run_pipeline (the
+    reference's per-iteration host fold) vs run_device_stream (the same fold on the device,
+    host chunks staged a block at a time on a copy stream). Both results must agree."""
+    px = 1 << 20
+    n = min(n, pinned.size // px)
+    words = pinned.view(np.uint32)
+    chunks = [hs.PackedChunk(words[i * (px // 4):(i + 1) * (px // 4)]) for i in range(n)]
+    cfg = hs.PipelineConfig(num_iterations=n, chunk_pixels=px, window_size=128)
+
+    def src():
+        for c in chunks:
+            yield [c]
+
+    out, res = {}, {}
+    for name, fn in (("run_pipeline", hs.run_pipeline), ("run_device_stream", hs.run_device_stream)):
+        fn(src(), cfg, hs.SwitchPolicy())  # warm-up pass
+        t0 = time.perf_counter()
+        res[name] = fn(src(), cfg, hs.SwitchPolicy())
+        out[name + "_gbs"] = round(n * px / (time.perf_counter() - t0) / 1e9, 3)
+    a, b = res["run_pipeline"], res["run_device_stream"]
+    assert a[0] == b[0] and a[1] == b[1] and a[3] == b[3], "device engine != host engine"
+    out.update({"bytes": n * px, "iterations": n, "chunk": "1 MiB pinned, batch 1, window 128",
+                "parity": "accumulator, window and kernel log equal between the two engines"})
+    return out

@@ -205,10 +205,61 @@ def test_device_stream_equals_host_engine_at_scale(cuda):
     assert hs.KernelKind.ADAPTIVE in dev[3] and dev[3][0] is hs.KernelKind.NAIVE
 
 
-def test_device_stream_rejects_host_chunks(cuda):
+def test_device_stream_rejects_foreign_chunks(cuda):
     cfg = small_cfg(num_iterations=2)
     with pytest.raises(TypeError):
-        hs.run_device_stream(uniform_source(cfg, 1), cfg, POLICY)
+        hs.run_device_stream(iter([[np.zeros(16, np.uint8)], [np.zeros(16, np.uint8)]]), cfg, POLICY)
+
+
+@pytest.mark.parametrize("kind", ["pageable", "pinned", "mixed"])
+def test_device_stream_from_host_chunks(cuda, golden, kind):
+    """Host PackedChunks through the device engine (staged a block at a time on a copy
+    stream one block ahead): the reference's own run_sequential results bit for bit --
+    pageable chunks (bounce buffer), page-locked ones (direct DMA) and blocks mixing host
+    and device chunks; small blocks force many staging-slot reuses."""
+    torch = cuda
+    from paper_1011_0235_b200 import device as D
+
+    def host_batches(m):
+        for j, batch in enumerate(schedule_stream(_segments(m), m["batch_size"])):
+            out = []
+            for k, c in enumerate(batch):
+                if kind == "pinned" or (kind == "mixed" and (j + k) % 3 == 1):
+                    w = D.pinned_words(c.words.size)
+                    w[:] = c.words
+                    out.append(hs.PackedChunk(w))
+                elif kind == "mixed" and (j + k) % 3 == 2:
+                    out.append(hs.DeviceChunk(torch.from_numpy(c.pixels().copy()).cuda()))
+                else:
+                    out.append(c)
+            yield out
+
+    for i, m in enumerate(golden.meta["streams"]):
+        cfg = hs.PipelineConfig(num_iterations=m["num_iterations"], chunk_pixels=m["chunk_pixels"],
+                                batch_size=m["batch_size"], recompute_pattern_every=m["recompute_pattern_every"],
+                                window_size=m["window_size"], worker=hs.WorkerGroupConfig(4, 2))
+        block = 3 * m["chunk_pixels"] * m["batch_size"]  # a few iterations per block
+        acc, win, rep, log = hs.run_device_stream(host_batches(m), cfg, POLICY, block_bytes=block)
+        assert [k.value for k in log] == m["kernel_log"], (kind, i)
+        per = np.stack([np.stack([h.counts for h in it]) for it in rep.per_slice_histograms])
+        assert np.array_equal(per, golden[f"stream_{i}_per_slice"]), (kind, i)
+        assert np.array_equal(acc.running.counts, golden[f"stream_{i}_acc"]) and acc.chunks_seen == m["chunks_seen"]
+        assert np.array_equal(win.windowed.counts, golden[f"stream_{i}_window"])
+        assert rep.degeneracy_log == golden[f"stream_{i}_deg"].tolist(), (kind, i)
+        assert rep.divergence_log == golden[f"stream_{i}_div"].tolist(), (kind, i)
+
+
+def test_device_stream_host_chunks_at_scale(cuda):
+    """1 MiB pageable chunks, batch 1 (the reference's default pipeline shape), 600
+    iterations in 64 MiB blocks: equal to run_sequential on the same source."""
+    px = 1 << 20
+    segs = [(hs.SourceSpec("uniform", px, 31), 250), (hs.SourceSpec("constant", px, 31, value=77), 150),
+            (hs.SourceSpec("normal", px, 31, mean=100.0, sigma=16.0), 200)]
+    cfg = hs.PipelineConfig(num_iterations=600, chunk_pixels=px, window_size=32)
+    seq = hs.run_sequential(schedule_stream(segs), cfg, POLICY)
+    dev = hs.run_device_stream(schedule_stream(segs), cfg, POLICY, block_bytes=64 << 20)
+    assert states_equal(seq, dev)
+    assert [k.value for k in seq[3]] == [k.value for k in dev[3]]
 
 
 @pytest.mark.parametrize("window,batch", [(1, 37), (4, 64), (15, 20), (16, 5), (16, 37), (23, 16), (32, 40), (33, 64), (64, 64)])
