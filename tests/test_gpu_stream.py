@@ -329,3 +329,26 @@ def test_pageable_batches_back_to_back_on_one_staging(cuda, oracle):
     assert np.array_equal(out1.cpu().numpy().view(np.uint64)[0], oracle.histogram(a))
     assert np.array_equal(out2.cpu().numpy().view(np.uint64)[0], oracle.histogram(b))
     assert np.array_equal(out3.cpu().numpy().view(np.uint64)[0], oracle.histogram(b))
+
+
+def test_device_stream_host_chunks_source_errors(cuda):
+    """A source that ends early or raises mid-run with host blocks staged: the
+    reference's exceptions propagate (SourceExhausted, the source's own error)."""
+    px = 1 << 16
+    cfg = hs.PipelineConfig(num_iterations=40, chunk_pixels=px, window_size=4)
+
+    def short():
+        for j in range(25):
+            yield [hs.generate(hs.SourceSpec("uniform", px, j))]
+
+    with pytest.raises(hs.SourceExhausted):
+        hs.run_device_stream(short(), cfg, POLICY, block_bytes=4 * px)
+
+    def broken():
+        for j in range(30):
+            if j == 17:
+                raise RuntimeError("source broke")
+            yield [hs.generate(hs.SourceSpec("uniform", px, j))]
+
+    with pytest.raises(RuntimeError, match="source broke"):
+        hs.run_device_stream(broken(), cfg, POLICY, block_bytes=4 * px)
