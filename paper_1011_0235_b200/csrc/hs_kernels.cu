@@ -1371,11 +1371,22 @@ __global__ void __launch_bounds__(256) k_block_commit(const __grid_constant__ Bl
   win[b] = pR - pe_at(local, tile_tot, max(0, R - W), b);
   // ring: push k of the block sits in slot (head + c0 + k) mod W; only the last W survive
   {
+    // 16 loads in flight per thread before their stores: one at a time, the copy of up to
+    // W rows was a chain of L2 round trips (77 us of a 256-chunk block's commit in ncu)
+    constexpr int kBatch = 16;
     const int j0 = max(0, m - W);
     int slot = int((uint32_t(head) + uint32_t(c0) + uint32_t(j0)) % uint32_t(W));
-    for (int j = j0; j < m; ++j) {
-      ring[size_t(slot) * 256 + b] = __ldcg(hist + size_t(j) * 256 + b);
-      slot = slot + 1 == W ? 0 : slot + 1;
+    for (int j = j0; j < m; j += kBatch) {
+      unsigned long long v[kBatch];
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u)
+        if (j + u < m) v[u] = __ldcg(hist + size_t(j + u) * 256 + b);
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u)
+        if (j + u < m) {
+          ring[size_t(slot) * 256 + b] = v[u];
+          slot = slot + 1 == W ? 0 : slot + 1;
+        }
     }
   }
   __shared__ double s_deg[kBlockMaxIter];
