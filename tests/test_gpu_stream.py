@@ -352,3 +352,49 @@ def test_device_stream_host_chunks_source_errors(cuda):
 
     with pytest.raises(RuntimeError, match="source broke"):
         hs.run_device_stream(broken(), cfg, POLICY, block_bytes=4 * px)
+
+
+def test_pipeline_resources_reused_after_errors(cuda):
+    # run_pipeline keeps its streams and readback staging per thread: a run that failed
+    # (source error, exhausted source) must leave them usable, and every later run exact
+    cfg = small_cfg(batch_size=3, num_iterations=6)
+    want = hs.run_sequential(uniform_source(cfg, 21), cfg, POLICY)
+
+    def broken():
+        yield [hs.generate(hs.SourceSpec("uniform", cfg.chunk_pixels, 5)) for _ in range(3)]
+        raise RuntimeError("source failure")
+
+    for _ in range(3):
+        with pytest.raises(RuntimeError, match="source failure"):
+            hs.run_pipeline(broken(), cfg, POLICY)
+        with pytest.raises(hs.SourceExhausted):
+            hs.run_pipeline(uniform_source(small_cfg(batch_size=3, num_iterations=2), 1), cfg, POLICY)
+        assert states_equal(hs.run_pipeline(uniform_source(cfg, 21), cfg, POLICY), want)
+
+
+def test_pipeline_concurrent_threads(cuda):
+    # each thread has its own streams and workspace: concurrent runs never share rows
+    import threading
+
+    cfgs = [small_cfg(batch_size=b, num_iterations=12, chunk_pixels=4096) for b in (1, 2, 3, 4)]
+    want = [hs.run_sequential(uniform_source(c, 30 + k), c, POLICY) for k, c in enumerate(cfgs)]
+    got, errors = [None] * len(cfgs), []
+
+    def worker(k):
+        try:
+            for _ in range(3):
+                got[k] = hs.run_pipeline(uniform_source(cfgs[k], 30 + k), cfgs[k], POLICY)
+                assert states_equal(got[k], want[k])
+        except BaseException as exc:  # reported by the main thread
+            errors.append(exc)
+
+    threads = [threading.Thread(target=worker, args=(k,)) for k in range(len(cfgs))]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert not errors, errors
+    from paper_1011_0235_b200 import stream as S
+
+    mine = S._pipeline_resources(__import__("torch"), 0)
+    assert mine is S._pipeline_resources(__import__("torch"), 0)  # made once per thread
