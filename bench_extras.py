@@ -129,7 +129,7 @@ def c1_image(hs, N, torch, dev):
             "graph_single_image_us": round(graph_us, 3), "cpu_reference_port_us": round(cpu_us, 1)}
 
 
-def c3_switch(hs, torch, dev):
+def c3_switch(hs, torch, dev, **engine_kw):
     """BASELINE configs[2]: a stream that turns degenerate -- 1 GiB uniform, then 1 GiB of
     a bimodal peak (50/50 of bytes 40 and 200; not a reference generator: uniform bytes
     < 128 map to 40, the rest to 200), then 2 GiB constant 127 -- in 16 MiB chunks,
@@ -165,10 +165,10 @@ def c3_switch(hs, torch, dev):
     batches = [[hs.DeviceChunk(buf[(i * per_iter + j) * px:(i * per_iter + j + 1) * px]) for j in range(per_iter)]
                for i in range(iters)]  # views built once, outside the timed call
 
-    hs.run_device_stream(iter(batches), cfg, hs.SwitchPolicy())
+    hs.run_device_stream(iter(batches), cfg, hs.SwitchPolicy(), **engine_kw)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    acc, _, rep, log = hs.run_device_stream(iter(batches), cfg, hs.SwitchPolicy())
+    acc, _, rep, log = hs.run_device_stream(iter(batches), cfg, hs.SwitchPolicy(), **engine_kw)
     wall = time.perf_counter() - t0
     uni = O.histogram_mt(buf[:4 * per_iter * px].cpu().numpy())
     bim = buf[4 * per_iter * px:8 * per_iter * px]

@@ -77,6 +77,32 @@ def test_block_engine_small_iterations_and_register_path(cuda, oracle):
     assert set(off[2].executed_log) == {"k_lane"}
 
 
+@pytest.mark.parametrize("ahead", [1, 2, None])
+def test_blocks_ahead_bounds_register_path_lag(cuda, ahead):
+    """Large iterations, one per block: with at most ``ahead`` blocks queued the host
+    issues block k only after block k - ahead finished, so the register path engages
+    within ``ahead`` blocks of the device's decision (with no bound a fast host may have
+    issued every block first). Counts, state and logs equal the host engine either way."""
+    torch = cuda
+    px = 16 << 20
+    segs = [(hs.SourceSpec("uniform", px, 9), 4), (hs.SourceSpec("constant", px, 9, value=77), 12)]
+    cfg = hs.PipelineConfig(num_iterations=16, chunk_pixels=px, window_size=2)
+    seq = hs.run_sequential(schedule_stream(segs), cfg, POLICY)
+    dev = hs.run_device_stream(_device_batches(torch, segs, 1), cfg, POLICY, block_bytes=px, blocks_ahead=ahead)
+    _equal(seq, dev)
+    assert dev[2].block_sizes == [1] * 16
+    ex = dev[2].executed_log
+    assert all(e == "k_lane" for e in ex[:5]), ex
+    if ahead is not None:
+        # the window is all-77 after iteration 5 (window 2), the decision for iteration 6
+        # is published by block 5's commit; block 5 + ahead is issued after it completed
+        first = 6 + ahead - 1
+        assert all(e == "k_lane<HOT bin 77>" for e in ex[first:]), ex
+    with pytest.raises(ValueError):
+        hs.run_device_stream(_device_batches(torch, segs[:1], 1), hs.PipelineConfig(num_iterations=4, chunk_pixels=px),
+                             POLICY, blocks_ahead=0)
+
+
 def test_step_abi_equals_block_abi(cuda):
     """hs_stream_step per iteration and one hs_stream_block over the same iterations
     leave identical state and logs."""

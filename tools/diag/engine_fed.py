@@ -14,6 +14,6 @@ hs.generate_device(hs.SourceSpec("uniform", n * px, 3), buf)
 batches = [[hs.DeviceChunk(buf[i * px:(i + 1) * px])] for i in range(n)]
 cfg = hs.PipelineConfig(num_iterations=n, chunk_pixels=px, window_size=128)
 for _ in range(2):
-    hs.run_device_stream(iter(batches), cfg, hs.SwitchPolicy(), block_bytes=256 << 20)
+    hs.run_device_stream(iter(batches), cfg, hs.SwitchPolicy(), block_bytes=256 << 20, blocks_ahead=None)
 torch.cuda.synchronize()
 print("ok")
