@@ -540,7 +540,7 @@ def main(argv=None):
         e2e, pinned = e2e_run(hs, torch, rank, world, lo, hi, shard, sh, args.e2e_steps)
 
     cpu = None
-    if rank == 0 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu:  # the CPU baseline is an N=1 measurement
         ref = cpu_reference_run(args.cpu_seconds)
         port = cpu_port_run(args.cpu_seconds)
         if ref is not None:
