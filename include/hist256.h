@@ -270,6 +270,13 @@ int hs_degeneracy(const uint64_t* h_counts, double* max_bin_fraction, int* argma
  * HS_ERR_INVALID_ARG when either histogram is empty (the reference's EmptyHistogram). */
 int hs_divergence(const uint64_t* h_a, const uint64_t* h_b, double* out);
 
+/* Host staging helper (no reference counterpart; the reference has no device): copy n
+ * bytes from pageable memory into page-locked memory with streaming stores, leaving no
+ * dirty lines in the CPU caches, so the DMA that reads the destination next reads DRAM
+ * at the link's rate instead of snooping them. Copies of >= 1 MiB are split over up to
+ * `threads` host threads (one thread copies ~15 GB/s, a quarter of the PCIe link). */
+int hs_copy_streaming(void* dst, const void* src, uint64_t n, int threads);
+
 /* ---- seeded generators (datagen.py:92-155; splitmix64, byte-exact) ------ */
 #define HS_GEN_UNIFORM 0
 #define HS_GEN_SEQUENTIAL 1

@@ -73,6 +73,7 @@ EXPORTED = (
     "hs_binning_pattern",
     "hs_degeneracy",
     "hs_divergence",
+    "hs_copy_streaming",
     "hs_generate_host",
     "hs_generate_device",
     "hs_stream_state_bytes",
@@ -124,6 +125,7 @@ _SIGNATURES = {
     "hs_binning_pattern": (_c.c_int, [_U64P, _I64, _I64, _I64P, _I64P]),
     "hs_degeneracy": (_c.c_int, [_U64P, _c.POINTER(_c.c_double), _c.POINTER(_c.c_int), _U64P]),
     "hs_divergence": (_c.c_int, [_U64P, _U64P, _c.POINTER(_c.c_double)]),
+    "hs_copy_streaming": (_c.c_int, [_P, _P, _U64, _c.c_int]),
     "hs_generate_host": (
         _c.c_int,
         [_c.c_int, _U64, _c.c_int, _c.c_double, _c.c_double, _c.c_double, _P, _U64, _c.c_int],

@@ -14,6 +14,9 @@
 #include <cstring>
 #include <thread>
 #include <vector>
+#if defined(__x86_64__)
+#include <immintrin.h>
+#endif
 
 #include "../../include/hist256.h"
 
@@ -165,6 +168,42 @@ int hs_divergence(const uint64_t* a, const uint64_t* b, double* out) {
   double d[256];
   for (int k = 0; k < 256; ++k) d[k] = std::fabs(double(a[k]) / da - double(b[k]) / db);
   *out = 0.5 * pairwise_sum(d, 256);
+  return HS_OK;
+}
+
+int hs_copy_streaming(void* dst, const void* src, uint64_t n, int threads) {
+  if (n == 0) return HS_OK;
+  if (!dst || !src) return HS_ERR_INVALID_ARG;
+  uint8_t* const d0 = static_cast<uint8_t*>(dst);
+  const uint8_t* const s0 = static_cast<const uint8_t*>(src);
+  parallel_for(n, threads, [d0, s0](uint64_t a, uint64_t b) {
+    uint8_t* d = d0 + a;
+    const uint8_t* s = s0 + a;
+    uint64_t m = b - a;
+#if defined(__x86_64__)
+    // head up to a 16-B aligned destination, then 64 B per step with streaming stores
+    // (movntdq: the lines go to memory without being left dirty in the CPU caches), tail
+    const uint64_t head = std::min<uint64_t>(m, (16 - (reinterpret_cast<uintptr_t>(d) & 15)) & 15);
+    std::memcpy(d, s, head);
+    d += head;
+    s += head;
+    m -= head;
+    for (; m >= 64; m -= 64, d += 64, s += 64) {
+      const __m128i x0 = _mm_loadu_si128(reinterpret_cast<const __m128i*>(s));
+      const __m128i x1 = _mm_loadu_si128(reinterpret_cast<const __m128i*>(s + 16));
+      const __m128i x2 = _mm_loadu_si128(reinterpret_cast<const __m128i*>(s + 32));
+      const __m128i x3 = _mm_loadu_si128(reinterpret_cast<const __m128i*>(s + 48));
+      _mm_stream_si128(reinterpret_cast<__m128i*>(d), x0);
+      _mm_stream_si128(reinterpret_cast<__m128i*>(d + 16), x1);
+      _mm_stream_si128(reinterpret_cast<__m128i*>(d + 32), x2);
+      _mm_stream_si128(reinterpret_cast<__m128i*>(d + 48), x3);
+    }
+    std::memcpy(d, s, m);
+    _mm_sfence();  // the streamed lines are in memory before the caller hands them to a DMA
+#else
+    std::memcpy(d, s, m);
+#endif
+  });
   return HS_OK;
 }
 

@@ -6,7 +6,8 @@ kernels through the C ABI (include/hist256.h); if CUDA or the library is missing
 every entry point raises (there is no CPU fallback).
 
 Data flow for one batch (the reference's batch_histograms, stream.py:260-316):
-  host PackedChunks --H2D (pinned: async; pageable: staged by the driver)--> one device
+  host PackedChunks --H2D (pinned: async; pageable: copied into a pinned bounce buffer with
+  threaded streaming stores, large batches piecewise with each piece DMA'd as it lands)--> one device
   staging buffer -> hs_histogram_batched (one launch, one segment per chunk) ->
   uint64[n, 256] on device --D2H 2 KiB per chunk--> read-only Histogram256 values.
 DeviceChunks skip the H2D: their tensors are segments of the same launch.
@@ -15,6 +16,7 @@ from __future__ import annotations
 
 import bisect
 import ctypes
+import os
 import threading
 import warnings
 import weakref
@@ -115,6 +117,54 @@ def pinned_words(n_words: int) -> np.ndarray:
 
 def is_pinned(arr: np.ndarray) -> bool:
     return _pinned.contains(arr.ctypes.data, arr.nbytes)
+
+
+# ------------------------------------------------------------------ pageable copies
+# Pageable chunks reach the device through a page-locked bounce buffer. Two things set
+# the rate (tools/diag/pageable_rate.py, pageable_small.py): one host thread copies
+# 15-26 GB/s, below the PCIe link (8 threads: 74-79 GB/s); and a DMA out of a bounce
+# buffer the CPU has just written through its caches runs at 14-20 GB/s. So copies use
+# streaming stores (hs_copy_streaming). Up to 16 MiB of pageable input per batch is
+# copied in one call split over native threads; larger batches go in 4 MiB pieces to a
+# pool of copy threads, each piece DMA'd as soon as it has landed while the pool copies
+# on (pageable run_pipeline 14 -> 47 GB/s; native-thread pieces on the staging thread
+# reached 38). The driver's own pageable copy runs ~11 GB/s.
+_COPY_POOLED_ABOVE = 16 << 20
+_COPY_PIECE = 4 << 20
+_COPY_SYNC_MIN = 8 << 20  # synchronous calls with less pageable input use the driver's copy
+_copy_pool = None
+_copy_pool_lock = threading.Lock()
+
+
+def copy_threads() -> int:
+    """Host threads for pageable -> page-locked copies (HS_COPY_THREADS overrides)."""
+    env = os.environ.get("HS_COPY_THREADS")
+    if env:
+        return max(1, int(env))
+    return max(1, min(8, (os.cpu_count() or 2) // 2))
+
+
+def _threads_for(n: int) -> int:
+    # measured per copy: 1 MiB fastest on 1 thread (40 us; 4: 53), 2-4 MiB on 4, 16 MiB on 8
+    return 1 if n < (2 << 20) else min(copy_threads(), 4 if n < (16 << 20) else 8)
+
+
+def _copy_into(dst: np.ndarray, src: np.ndarray, threads: int = 1) -> None:
+    """dst[:] = src with streaming stores over up to ``threads`` host threads
+    (hs_copy_streaming; ctypes drops the GIL for the call)."""
+    N.check(N.lib().hs_copy_streaming(dst.ctypes.data, src.ctypes.data, src.nbytes, int(threads)),
+            "hs_copy_streaming")
+
+
+def _pool():
+    global _copy_pool
+    if _copy_pool is None:
+        with _copy_pool_lock:
+            if _copy_pool is None:
+                from concurrent.futures import ThreadPoolExecutor
+
+                _copy_pool = ThreadPoolExecutor(max_workers=copy_threads(), thread_name_prefix="hs-h2d-copy")
+    return _copy_pool
 
 
 # ------------------------------------------------------------------ staging
@@ -318,24 +368,46 @@ def stage(chunks: Sequence, staging: Staging | None, stream=None) -> StagedBatch
                     runs.append([hp, off, n, c.words])
                 keep.append(c.words)
             off += n
+        srcs = []  # (device offset, bytes, host array, page-locked?) per run
+        for hp, doff, n, first in runs:
+            if n == first.nbytes:
+                arr = first.view(np.uint8)
+            else:  # the run spans several chunks' memory (all kept alive above)
+                arr = np.ctypeslib.as_array((ctypes.c_uint8 * n).from_address(hp))
+            srcs.append((doff, n, arr, _pinned.contains(hp, n)))
+        pageable = sum(n for _, n, _, pinned in srcs if not pinned)
+        pool = _pool() if pageable > _COPY_POOLED_ABOVE else None
+        if pageable:
+            bounce = staging.host_bounce(total)
+            if staging._bounce_done is not None:  # its previous DMA must have read it
+                staging._bounce_done.synchronize()
+        jobs: list = []  # (device offset, page-locked source, pool future or None), in DMA order
+        try:
+            for doff, n, arr, pinned in srcs:
+                if pinned:
+                    jobs.append((doff, arr, None))
+                elif pool is not None:
+                    for a in range(0, n, _COPY_PIECE):
+                        dst = bounce[doff + a:doff + min(n, a + _COPY_PIECE)]
+                        jobs.append((doff + a, dst, pool.submit(_copy_into, dst, arr[a:a + _COPY_PIECE])))
+                else:
+                    jobs.append((doff, bounce[doff:doff + n], (arr, _threads_for(n))))
+            with t.cuda.stream(stream), warnings.catch_warnings():
+                warnings.simplefilter("ignore", UserWarning)  # chunks are read-only; torch only reads them
+                for doff, src_arr, job in jobs:
+                    if isinstance(job, tuple):  # copied here, over native threads
+                        _copy_into(src_arr, job[0], job[1])
+                    elif job is not None:
+                        job.result()  # this piece is in the bounce buffer: DMA it now
+                    src = t.from_numpy(src_arr)
+                    dev[doff:doff + src_arr.size].copy_(src, non_blocking=True)
+                    keep.append(src)
+        except BaseException:
+            for _, _, job in jobs:  # no pool copy may still write the bounce buffer after this
+                if job is not None and not isinstance(job, tuple):
+                    job.cancel() or job.exception()
+            raise
         with t.cuda.stream(stream):
-            for hp, doff, n, first in runs:
-                if n == first.nbytes:
-                    arr = first.view(np.uint8)
-                else:  # the run spans several chunks' memory (all kept alive above)
-                    arr = np.ctypeslib.as_array((ctypes.c_uint8 * n).from_address(hp))
-                if not _pinned.contains(hp, n):
-                    if bounce is None:
-                        bounce = staging.host_bounce(total)
-                        if staging._bounce_done is not None:  # its previous DMA must have read it
-                            staging._bounce_done.synchronize()
-                    np.copyto(bounce[doff:doff + n], arr)
-                    arr = bounce[doff:doff + n]
-                with warnings.catch_warnings():  # chunks are read-only views; torch only reads them
-                    warnings.simplefilter("ignore", UserWarning)
-                    src = t.from_numpy(arr)
-                dev[doff:doff + n].copy_(src, non_blocking=True)
-                keep.append(src)
             ready = t.cuda.Event()
             ready.record(stream)
             if bounce is not None:
@@ -454,10 +526,17 @@ def histograms(chunks: Sequence, kind: int, pattern=None, impl: int = N.HS_IMPL_
     """Synchronous batched histograms of host/device chunks -> uint64 [n, 256]."""
     t = require_cuda()
     st = default_staging()
+    all_host = bool(chunks) and all(type(c) is PackedChunk for c in chunks)
+    if all_host and _pageable_bytes(chunks) >= _COPY_SYNC_MIN:
+        # >= 8 MiB of pageable host memory: threaded streaming copies into the bounce
+        # buffer and their DMAs beat the driver's pageable copy (16 MiB 0.66 vs 0.78 ms,
+        # 64 MiB 1.9 vs 4.7 ms); below that the driver's copy is as fast
+        stream = t.cuda.current_stream()
+        return _sync_histograms(stage(chunks, st, stream), kind, pattern, impl, st, stream)
     if len(chunks) == 1 and type(chunks[0]) in (PackedChunk, DeviceChunk):
         return _one_histogram(chunks[0], kind, pattern, impl, st)[None, :]
     stream = t.cuda.current_stream()
-    if chunks and all(type(c) is PackedChunk for c in chunks):
+    if all_host:
         return _host_histograms(chunks, kind, pattern, impl, st, stream)
     if chunks and all(type(c) is DeviceChunk for c in chunks):
         staged = stage(chunks, st, stream)
@@ -465,6 +544,10 @@ def histograms(chunks: Sequence, kind: int, pattern=None, impl: int = N.HS_IMPL_
     staged = stage(chunks, st, stream)
     out = launch(staged, kind, pattern, stream, impl, staging=st)
     return readback(out, st, stream)
+
+
+def _pageable_bytes(chunks) -> int:
+    return sum(c.byte_size for c in chunks if c.byte_size and not is_pinned(c.words))
 
 
 def _raw_stream(index: int) -> int:

@@ -398,3 +398,58 @@ def test_pipeline_concurrent_threads(cuda):
 
     mine = S._pipeline_resources(__import__("torch"), 0)
     assert mine is S._pipeline_resources(__import__("torch"), 0)  # made once per thread
+
+
+@pytest.mark.parametrize("sizes,pinned_mask", [
+    ([3 << 20], [False]),                                  # one run, pieces shared by the pool, one DMA
+    ([(1 << 20) + 4, 4, (5 << 20) - 12, 0, 12], [False] * 5),  # ragged runs, an empty chunk
+    ([20 << 20, (9 << 20) + 4096 + 8], [False, False]),    # > 16 MiB: 4 MiB pieces, DMA per piece
+    ([6 << 20, 6 << 20, 6 << 20], [False, True, False]),   # pinned run between pageable ones
+])
+def test_pageable_batches_through_copy_pool(cuda, oracle, sizes, pinned_mask):
+    """Pageable host chunks of >= 2 MiB per batch are copied into the bounce buffer by the
+    host copy pool (pieces DMA'd as they land); counts exact per chunk, through stage()
+    and through the synchronous API (naive_histogram / batch_histograms)."""
+    torch = cuda
+    from paper_1011_0235_b200 import device as D
+
+    rng = np.random.default_rng(sum(sizes))
+    chunks, want = [], []
+    for k, (n, pin) in enumerate(zip(sizes, pinned_mask)):
+        b = oracle.generate("normal", n, 40 + k, mean=float(rng.uniform(20, 230)), sigma=9.0) if n else \
+            np.zeros(0, np.uint8)
+        if pin:
+            p = D.pinned_bytes(n)
+            p[:] = b
+            b = p
+        chunks.append(hs.PackedChunk(b.view(np.uint32)))
+        want.append(oracle.histogram(b))
+    st = D.Staging()
+    stream = torch.cuda.current_stream()
+    staged = D.stage(chunks, st, stream)
+    out = D.launch(staged, 0, None, stream, staging=st)
+    got = out.cpu().numpy().view(np.uint64)
+    for k in range(len(chunks)):
+        assert np.array_equal(got[k], want[k]), k
+    got = hs.batch_histograms(chunks, hs.KernelKind.NAIVE, None, SMALL)
+    assert [h.counts.tolist() for h in got] == [w.tolist() for w in want]
+    big = max(range(len(chunks)), key=lambda k: sizes[k])
+    assert np.array_equal(hs.naive_histogram(chunks[big], SMALL).counts, want[big])
+
+
+def test_pageable_pipeline_through_copy_pool(cuda, oracle):
+    """run_pipeline on pageable 4 MiB chunks, batches of 8 (32 MiB per batch through the
+    pool): accumulator exact and equal to run_sequential."""
+    px, batch, iters = 4 << 20, 8, 6
+    data = oracle.generate("uniform", px * batch * iters, 77)
+    words = data.view(np.uint32)
+    chunks = [hs.PackedChunk(words[i * (px // 4):(i + 1) * (px // 4)].copy()) for i in range(batch * iters)]
+    cfg = hs.PipelineConfig(num_iterations=iters, chunk_pixels=px, batch_size=batch, window_size=3)
+
+    def src():
+        for i in range(iters):
+            yield chunks[i * batch:(i + 1) * batch]
+
+    pipe = hs.run_pipeline(src(), cfg, POLICY)
+    assert np.array_equal(pipe[0].running.counts, oracle.histogram(data))
+    assert states_equal(pipe, hs.run_sequential(src(), cfg, POLICY))

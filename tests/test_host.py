@@ -329,3 +329,18 @@ def test_bench_relaunches_itself_under_torchrun(monkeypatch):
     assert cmd[1:3] == ["-m", "torch.distributed.run"] and "--nproc-per-node=4" in cmd
     assert cmd[cmd.index("--master-addr") + 1] == "127.0.0.1"
     assert cmd[-6:] == ["--gpus", "4", "--steps", "7", "--warmup", "3"]
+
+
+def test_copy_streaming_exact():
+    """hs_copy_streaming (the pageable -> page-locked staging copy) at every head/tail
+    alignment and size class; no byte outside the destination is touched."""
+    from paper_1011_0235_b200 import device as D
+
+    for n in (0, 1, 15, 16, 17, 63, 64, 65, 127, 1000, 4096 + 7, (1 << 20) + 3):
+        src = np.random.default_rng(n).integers(0, 256, n + 3, dtype=np.uint8)
+        for so in (0, 1, 3):
+            for do in (0, 5, 16):
+                dst = np.zeros(n + 24, np.uint8)
+                D._copy_into(dst[do:do + n], src[so:so + n])
+                assert np.array_equal(dst[do:do + n], src[so:so + n]), (n, so, do)
+                assert not dst[:do].any() and not dst[do + n:].any(), (n, so, do)
