@@ -59,7 +59,7 @@ constexpr size_t kTicketBytes = 1024;  // per call slot: kMaxSeg u32 tickets
 #endif
 constexpr int kCallSlots = HS_CALL_SLOTS;
 constexpr size_t kWsHeadBytes = HS_WS_HEAD_BYTES;
-// Every rotating call adds exactly kArrive to the header's call counter (claim_slot);
+// Every rotating call adds exactly kArrive to the header's call counter (claim_and_probe_warp0);
 // grids must stay below it.
 constexpr unsigned long long kArrive = 4096;
 constexpr uint64_t kBigCap = 1ull << 30;  // u32 per-warp counters: far from wrapping
@@ -416,19 +416,32 @@ __device__ __forceinline__ void set_slot(const Tickets& tk, uint32_t slot, SlotV
   sv.acc = reinterpret_cast<unsigned long long*>(base + kTicketBytes);
 }
 
-// thread 0 of every CTA of a rotating call, before it triggers: arrive (CTA 0 adds
-// kArrive - grid + 1, the others 1, so the counter moves by kArrive per call and the
-// value returned to any CTA of the call, over kArrive, is the call's number n)
-__device__ __forceinline__ void claim_slot(const Tickets& tk, SlotView& sv) {
-  const unsigned long long n =
-      atomicAdd(&tk.hdr->calls, blockIdx.x == 0 ? kArrive - gridDim.x + 1 : 1ull) / kArrive;
-  set_slot(tk, uint32_t(n % kCallSlots), sv);
-  sv.epoch = uint32_t(n / kCallSlots);
-}
-
-// read once the next launch is let in, looked at by the first flush: by then it is back
-__device__ __forceinline__ void probe_slot(const Tickets& tk, SlotView& sv) {
-  sv.probe = ld_relaxed_u32(&tk.hdr->drained[sv.slot]);
+// warp 0 of every CTA of a rotating call, before it triggers. Lane 0 arrives on the call
+// counter (CTA 0 adds kArrive - grid + 1, the others 1, so the counter moves by kArrive
+// per call and the value returned to any CTA of the call, over kArrive, is the call's
+// number n, which names its slot and epoch) while lanes 0..K-1 read
+// every slot's drained word, so the probe's round trip overlaps the arrival's instead of
+// following it (tools/trace_lane.py: wait return -> loop begin 1.4 us, two round trips).
+// Reading drained[] before the claim is returned is sound: the word only reaches the
+// call's epoch through the release of the slot's previous user, never beyond it before
+// this call releases it, so probe == epoch still means "released" (await_slot), and an
+// older value only sends await_slot to its acquire loop. lane 0 then lets the next
+// launch in; the first flush looks at sv.probe.
+__device__ __forceinline__ void claim_and_probe_warp0(const Tickets& tk, SlotView& sv) {
+  const uint32_t lane = threadIdx.x & 31;
+  const unsigned int d = lane < uint32_t(kCallSlots) ? ld_relaxed_u32(&tk.hdr->drained[lane]) : 0u;
+  unsigned long long n = 0;
+  if (lane == 0)
+    n = atomicAdd(&tk.hdr->calls, blockIdx.x == 0 ? kArrive - gridDim.x + 1 : 1ull) / kArrive;
+  n = __shfl_sync(0xffffffffu, n, 0);
+  const uint32_t slot = uint32_t(n % kCallSlots);
+  const unsigned int probe = __shfl_sync(0xffffffffu, d, slot);
+  if (lane == 0) {
+    set_slot(tk, slot, sv);
+    sv.epoch = uint32_t(n / kCallSlots);
+    pdl_launch_dependents();
+    sv.probe = probe;
+  }
 }
 
 // thread 0, before the CTA's first RED into a rotating slot: every earlier call on the
@@ -663,7 +676,7 @@ __global__ void __launch_bounds__(TH, MB)
   // A call's first launch waits for its stream predecessor before loading (round 2 A/B,
   // profiles/r2_first_launch_ab.txt: waiting first, then letting the next launch in, was
   // the fastest safe order). A rotating call's CTAs let the next launch in only after
-  // arriving on the workspace's call counter (claim_slot), which orders the calls' slots.
+  // arriving on the workspace's call counter (claim_and_probe_warp0), which orders the calls' slots.
   if (wait_first) pdl_wait();
   const bool ticketed = tk.hdr != nullptr;
   const bool rotating = ticketed && tk.rotate;
@@ -673,14 +686,9 @@ __global__ void __launch_bounds__(TH, MB)
   // take effect); a rotating call's CTAs trigger from thread 0 only, after its arrival
   // is back, so that every CTA of the call arrives before any CTA of the next one.
   if (!rotating) pdl_launch_dependents();
+  if (rotating && threadIdx.x < 32) claim_and_probe_warp0(tk, sv);
   if (threadIdx.x == 0) {
-    if (rotating) {
-      claim_slot(tk, sv);
-      pdl_launch_dependents();
-      probe_slot(tk, sv);
-    } else if (ticketed) {
-      set_slot(tk, kCallSlots, sv);
-    }
+    if (ticketed && !rotating) set_slot(tk, kCallSlots, sv);
     int n = 0;
     for_each_piece<~0ull>(sp, [&](int s, uint64_t p0, uint64_t p1) {
       pc_p0[n] = p0;

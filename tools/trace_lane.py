@@ -73,3 +73,8 @@ print(f"  CTA exit spread: p10 {np.percentile(ex, 10):.1f} p50 {np.percentile(ex
 sm = np.array([0] * g)
 hist = np.histogram(rel[:, 0], bins=8)
 print("  CTA start histogram (us edges, counts):", [round(e, 1) for e in hist[1]], hist[0].tolist())
+if (t[:, 14] > 0).any():  # instrumented with a stamp after the first-launch wait (waiting calls)
+    w = rel[:, 14]
+    print(f"  wait return: min {w.min():.2f} max {w.max():.2f} us; wait return -> last exit {rel[:, 15].max() - w.min():.2f} us")
+    print(f"  wait return -> loop begin median {np.median(rel[:, 1] - w):.2f} us; loop median {np.median(rel[:, 2] - rel[:, 1]):.2f} us")
+    per = None
