@@ -395,11 +395,6 @@ struct SlotView {
   uint32_t slot, epoch, probe;  // probe: drained[slot] as read after the claim
 };
 
-__device__ __forceinline__ unsigned int ld_relaxed_u32(const unsigned int* p) {
-  unsigned int v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
 __device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
   unsigned int v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -419,7 +414,7 @@ __device__ __forceinline__ void set_slot(const Tickets& tk, uint32_t slot, SlotV
 // warp 0 of every CTA of a rotating call, before it triggers. Lane 0 arrives on the call
 // counter (CTA 0 adds kArrive - grid + 1, the others 1, so the counter moves by kArrive
 // per call and the value returned to any CTA of the call, over kArrive, is the call's
-// number n, which names its slot and epoch) while lanes 0..K-1 read
+// number n, which names its slot and epoch) while lanes 1..K read (acquire)
 // every slot's drained word, so the probe's round trip overlaps the arrival's instead of
 // following it (tools/trace_lane.py: wait return -> loop begin 1.4 us, two round trips).
 // Reading drained[] before the claim is returned is sound: the word only reaches the
@@ -429,13 +424,15 @@ __device__ __forceinline__ void set_slot(const Tickets& tk, uint32_t slot, SlotV
 // launch in; the first flush looks at sv.probe.
 __device__ __forceinline__ void claim_and_probe_warp0(const Tickets& tk, SlotView& sv) {
   const uint32_t lane = threadIdx.x & 31;
-  const unsigned int d = lane < uint32_t(kCallSlots) ? ld_relaxed_u32(&tk.hdr->drained[lane]) : 0u;
   unsigned long long n = 0;
-  if (lane == 0)
-    n = atomicAdd(&tk.hdr->calls, blockIdx.x == 0 ? kArrive - gridDim.x + 1 : 1ull) / kArrive;
-  n = __shfl_sync(0xffffffffu, n, 0);
+  if (lane == 0) n = atomicAdd(&tk.hdr->calls, blockIdx.x == 0 ? kArrive - gridDim.x + 1 : 1ull);
+  // lanes 1..K acquire drained[lane - 1] (issued behind the arrival, not ordered before it:
+  // an acquire orders only its own thread's later accesses, and lane 0 is not among them)
+  const unsigned int d =
+      (lane >= 1 && lane <= uint32_t(kCallSlots)) ? ld_acquire_u32(&tk.hdr->drained[lane - 1]) : 0u;
+  n = __shfl_sync(0xffffffffu, n, 0) / kArrive;
   const uint32_t slot = uint32_t(n % kCallSlots);
-  const unsigned int probe = __shfl_sync(0xffffffffu, d, slot);
+  const unsigned int probe = __shfl_sync(0xffffffffu, d, slot + 1);
   if (lane == 0) {
     set_slot(tk, slot, sv);
     sv.epoch = uint32_t(n / kCallSlots);
@@ -445,13 +442,10 @@ __device__ __forceinline__ void claim_and_probe_warp0(const Tickets& tk, SlotVie
 }
 
 // thread 0, before the CTA's first RED into a rotating slot: every earlier call on the
-// slot has released it (the probe saw the release store, with the fence making it an
-// acquire, or the acquire loop does)
+// slot has released it (the prologue's acquire saw the release store -- the barrier
+// before the flush carries that to every thread's REDs -- or the acquire loop does)
 __device__ __forceinline__ void await_slot(const Tickets& tk, SlotView& sv) {
-  if (sv.probe == sv.epoch) {
-    __threadfence();
-    return;
-  }
+  if (sv.probe == sv.epoch) return;  // acquired in the prologue (claim_and_probe_warp0)
   while (ld_acquire_u32(&tk.hdr->drained[sv.slot]) != sv.epoch) __nanosleep(64);
   sv.probe = sv.epoch;
 }
