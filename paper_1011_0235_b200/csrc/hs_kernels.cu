@@ -497,8 +497,10 @@ __device__ __forceinline__ void release_slot(const Tickets& tk, const SlotView& 
 
 // End of a ticketed CTA that flushed segments [s_first, s_last] into their accumulator
 // rows: one fence, then a ticket per segment; the last CTA of a segment takes the row
-// with atomicExch(.., 0) (reading and re-zeroing it), stores the output row and resets
-// the ticket, so the slot's rows and tickets are zero again when the call ends.
+// with atomicExch(.., 0) (reading and re-zeroing it) and stores the output row. Tickets
+// are atomicInc with the segment's last ticket as the wrap limit, so the last CTA's
+// ticket returns the counter to zero by itself: no reset store for the slot's release
+// fence to wait on, and the slot's rows and tickets are zero again when the call ends.
 // stage: the CTA's 32 KB counter array, free after its last flush (16 rows of u64[256])
 constexpr int kStageRows = 16;
 __device__ __forceinline__ void lane_tickets(const Tickets& tk, const SlotView& sv, const SegParams& sp, int s_first,
@@ -511,20 +513,21 @@ __device__ __forceinline__ void lane_tickets(const Tickets& tk, const SlotView& 
   if (threadIdx.x == 0) {
     int m = 0;
     if (sp.merge) {
-      if (atomicAdd(sv.ticket + sp.acc_base, 1u) == sp.merge_ctas) last_seg[m++] = 0;
+      if (atomicInc(sv.ticket + sp.acc_base, sp.merge_ctas) == sp.merge_ctas) last_seg[m++] = 0;
       s_last = -1;  // no per-segment tickets
     }
     for (int s = s_first; s <= s_last; ++s) {
       if (sp.vstart[s + 1] == sp.vstart[s]) continue;  // empty: no CTA owns it
       if ((sp.open_mask[s >> 5] >> (s & 31)) & 1) continue;  // finalized by a later launch
-      if (atomicAdd(sv.ticket + sp.acc_base + s, 1u) == sp.ctas_after_first[s]) last_seg[m++] = s;
+      if (atomicInc(sv.ticket + sp.acc_base + s, sp.ctas_after_first[s]) == sp.ctas_after_first[s])
+        last_seg[m++] = s;
     }
     n_last = m;
+    if (m) __threadfence();  // acquire: the other CTAs' REDs (the barrier below carries it to every thread)
   }
   __syncthreads();
   const int m = n_last;
   if (!m) return;
-  __threadfence();
   // The output is what this call shares with its predecessor on the stream (the same
   // buffer, or one the predecessor reads): it is stored only once that one is complete
   // (griddepcontrol.wait; serial calls have waited before their first RED). A rotating
@@ -535,7 +538,6 @@ __device__ __forceinline__ void lane_tickets(const Tickets& tk, const SlotView& 
       const int s = last_seg[k];
       for (uint32_t b = threadIdx.x; b < 256; b += blockDim.x)
         stage[k * 256 + b] = atomicExch(sv.acc + size_t(sp.acc_base + s) * 256 + b, 0ull);
-      if (threadIdx.x == 0) sv.ticket[sp.acc_base + s] = 0;
     }
     __syncthreads();
     release_slot(tk, sv, m);
@@ -550,7 +552,6 @@ __device__ __forceinline__ void lane_tickets(const Tickets& tk, const SlotView& 
     const int s = last_seg[k];
     for (uint32_t b = threadIdx.x; b < 256; b += blockDim.x)
       out[size_t(sp.out_base + s) * 256 + b] = atomicExch(sv.acc + size_t(sp.acc_base + s) * 256 + b, 0ull);
-    if (threadIdx.x == 0) sv.ticket[sp.acc_base + s] = 0;
   }
   if (tk.rotate) {
     __syncthreads();
