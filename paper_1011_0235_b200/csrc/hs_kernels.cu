@@ -1947,7 +1947,7 @@ int histogram_batched(const uint8_t* d_data, const uint64_t* h_begin, const uint
     // a merged call over several groups finalizes once, in its last group: serial. So
     // are the blocking entries (latency): the host waits for each call, so there is no
     // next call to overlap and the arrival would only add its round trip.
-    if (merge && nseg <= group && !latency) plan_call(tk, h_begin, h_end, 0, nseg, true);
+    if (merge && nseg <= group && !latency && !wait_first) plan_call(tk, h_begin, h_end, 0, nseg, true);
   } else {
     cudaError_t e = cudaMemsetAsync(d_out, 0, size_t(merge ? 1 : nseg) * 256 * sizeof(uint64_t), st);
     if (e != cudaSuccess) return fold(e);
@@ -1969,7 +1969,11 @@ int histogram_batched(const uint8_t* d_data, const uint64_t* h_begin, const uint
       if (e != cudaSuccess) return fold(e);
       continue;
     }
-    if (!merge && !latency) plan_call(tk, h_begin, h_end, s0, ns, false);  // each group is a call of its own
+    // each group is a call of its own. A call that waits for its predecessor before
+    // loading (the default) gains nothing from a rotating slot -- the predecessor is
+    // complete before any of its CTAs counts -- and would only add the arrival's round
+    // trip, so it keeps the serial slot, as the blocking entries do.
+    if (!merge && !latency && !wait_first) plan_call(tk, h_begin, h_end, s0, ns, false);
     rc = launch_segments(d_data, h_begin, h_end, s0, ns, kind, impl, have_pattern ? &pp : nullptr,
                          reinterpret_cast<unsigned long long*>(d_out), st, di, tk, 0, latency, wait_first, merge,
                          last_busy < s0 + ns);
