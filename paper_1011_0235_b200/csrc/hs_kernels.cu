@@ -58,6 +58,7 @@ constexpr size_t kTicketBytes = 1024;  // per call slot: kMaxSeg u32 tickets
 #define HS_CALL_SLOTS HS_WS_SLOTS
 #endif
 constexpr int kCallSlots = HS_CALL_SLOTS;
+static_assert(kCallSlots >= 1 && kCallSlots <= 31, "warp 0's lanes 1..K probe the slots");
 constexpr size_t kWsHeadBytes = HS_WS_HEAD_BYTES;
 // Every rotating call adds exactly kArrive to the header's call counter (claim_and_probe_warp0);
 // grids must stay below it.
