@@ -343,6 +343,7 @@ __device__ __forceinline__ EachVec<U, VecFn> each_vec(VecFn& f) { return EachVec
 constexpr int kLaneThreads = HS_LANE_THREADS;
 constexpr int kLaneBlocks = HS_LANE_BLOCKS;
 constexpr int kLaneHotThreads = 768;
+static_assert(kMaxSeg <= kLaneHotThreads && kMaxSeg <= kLaneThreads, "one ticket-taking thread per segment");
 constexpr int kLaneMinBlocks = 2;  // HOT form
 constexpr uint32_t kLaneArrayBytes = 256 * 32 * 4;
 
@@ -509,22 +510,27 @@ __device__ __forceinline__ void lane_tickets(const Tickets& tk, const SlotView& 
   __shared__ int last_seg[kMaxSeg];
   __shared__ int n_last;
   if (sp.merge && !sp.merge_final) return;  // a later launch of the call finalizes the row
+  if (threadIdx.x == 0) n_last = 0;
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int m = 0;
-    if (sp.merge) {
-      if (atomicInc(sv.ticket + sp.acc_base, sp.merge_ctas) == sp.merge_ctas) last_seg[m++] = 0;
-      s_last = -1;  // no per-segment tickets
+  // one ticket per segment, taken by thread (s - s_first) so that a CTA spanning several
+  // segments pays one round trip, not one per segment; a thread that draws a segment's
+  // last ticket fences (acquire: the other CTAs' REDs) before the barrier carries it to
+  // every thread
+  if (sp.merge) {
+    if (threadIdx.x == 0 && atomicInc(sv.ticket + sp.acc_base, sp.merge_ctas) == sp.merge_ctas) {
+      __threadfence();
+      last_seg[0] = 0;
+      n_last = 1;
     }
-    for (int s = s_first; s <= s_last; ++s) {
-      if (sp.vstart[s + 1] == sp.vstart[s]) continue;  // empty: no CTA owns it
-      if ((sp.open_mask[s >> 5] >> (s & 31)) & 1) continue;  // finalized by a later launch
-      if (atomicInc(sv.ticket + sp.acc_base + s, sp.ctas_after_first[s]) == sp.ctas_after_first[s])
-        last_seg[m++] = s;
+  } else if (s_first + int(threadIdx.x) <= s_last) {
+    const int s = s_first + int(threadIdx.x);
+    if (sp.vstart[s + 1] != sp.vstart[s] &&                 // empty: no CTA owns it
+        !((sp.open_mask[s >> 5] >> (s & 31)) & 1) &&        // open: finalized by a later launch
+        atomicInc(sv.ticket + sp.acc_base + s, sp.ctas_after_first[s]) == sp.ctas_after_first[s]) {
+      __threadfence();
+      last_seg[atomicAdd(&n_last, 1)] = s;
     }
-    n_last = m;
-    if (m) __threadfence();  // acquire: the other CTAs' REDs (the barrier below carries it to every thread)
   }
   __syncthreads();
   const int m = n_last;
