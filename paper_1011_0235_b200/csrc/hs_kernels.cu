@@ -539,32 +539,27 @@ __device__ __forceinline__ void lane_tickets(const Tickets& tk, const SlotView& 
   // buffer, or one the predecessor reads): it is stored only once that one is complete
   // (griddepcontrol.wait; serial calls have waited before their first RED). A rotating
   // slot is drained and released before that wait, so later calls can take it meanwhile.
-  // The rows are taken over the whole CTA (row k, bin b = item i's k * 256 + b), two
-  // exchanges in flight per thread, so m rows cost ~m * 256 / (2 * blockDim) round
-  // trips instead of m.
-  const uint32_t items = uint32_t(m) * 256;
-  auto take = [&](auto&& put) {
-    for (uint32_t i0 = threadIdx.x; i0 < items; i0 += 2 * blockDim.x) {
-      const uint32_t i1 = i0 + blockDim.x;
-      const unsigned long long v0 = atomicExch(sv.acc + size_t(sp.acc_base + last_seg[i0 >> 8]) * 256 + (i0 & 255), 0ull);
-      unsigned long long v1 = 0;
-      if (i1 < items) v1 = atomicExch(sv.acc + size_t(sp.acc_base + last_seg[i1 >> 8]) * 256 + (i1 & 255), 0ull);
-      put(i0, v0);
-      if (i1 < items) put(i1, v1);
-    }
-  };
   if (tk.rotate && m <= kStageRows) {
     unsigned long long* stage = reinterpret_cast<unsigned long long*>(stage_words);
-    take([&](uint32_t i, unsigned long long v) { stage[i] = v; });
+    for (int k = 0; k < m; ++k) {
+      const int s = last_seg[k];
+      for (uint32_t b = threadIdx.x; b < 256; b += blockDim.x)
+        stage[k * 256 + b] = atomicExch(sv.acc + size_t(sp.acc_base + s) * 256 + b, 0ull);
+    }
     __syncthreads();
     release_slot(tk, sv, m);
     pdl_wait();
-    for (uint32_t i = threadIdx.x; i < items; i += blockDim.x)
-      out[size_t(sp.out_base + last_seg[i >> 8]) * 256 + (i & 255)] = stage[i];
+    for (int k = 0; k < m; ++k)
+      for (uint32_t b = threadIdx.x; b < 256; b += blockDim.x)
+        out[size_t(sp.out_base + last_seg[k]) * 256 + b] = stage[k * 256 + b];
     return;
   }
   pdl_wait();
-  take([&](uint32_t i, unsigned long long v) { out[size_t(sp.out_base + last_seg[i >> 8]) * 256 + (i & 255)] = v; });
+  for (int k = 0; k < m; ++k) {
+    const int s = last_seg[k];
+    for (uint32_t b = threadIdx.x; b < 256; b += blockDim.x)
+      out[size_t(sp.out_base + s) * 256 + b] = atomicExch(sv.acc + size_t(sp.acc_base + s) * 256 + b, 0ull);
+  }
   if (tk.rotate) {
     __syncthreads();
     release_slot(tk, sv, m);
