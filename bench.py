@@ -508,7 +508,7 @@ def main(argv=None):
                 "algorithmic_bytes_per_launch": int(per_launch_bytes),
                 "achieved_method": (f"rank-0 timed region / {n_launch} launches ({launches_per_step} chained 1 GiB "
                                     "launches per step, back to back; k_lane is >99% of the step's GPU time, "
-                                    "profiles/r2z_launches_summary.txt)"),
+                                    "profiles/r2end_launches_summary.txt)"),
                 "avg_launch_ms": round(launch_ms, 5),
                 # a 1-byte-read kernel's ceiling: a read-only grid-stride stream reaches this
                 "read_only_ceiling_gbs": READ_ONLY_CEILING_GBS,
