@@ -9,7 +9,8 @@ Checked here, all against the oracle's counts and with the workspace clean after
   ADAPTIVE register path, chained and waiting first launches;
 - many calls writing the SAME output buffer: the last call's counts win;
 - a torch kernel that reads a call's output right behind it on the stream;
-- the call counter and drain counts of the header after N calls.
+- the call counter and drain counts of the header after N calls;
+- waiting (unflagged) calls take the serial slot, interleaved with chained ones.
 """
 import numpy as np
 import pytest
@@ -146,4 +147,32 @@ def test_slot_rotation_counts(stream_data):
     assert int(head[:8].view(np.uint64)[0]) == ncalls * 4096
     drained = head[WS_DRAINED].view(np.uint32).tolist()
     assert drained == [ncalls // SLOTS + (1 if j < ncalls % SLOTS else 0) for j in range(SLOTS)]
+    assert ws_clean(ws)
+
+
+def test_waiting_calls_take_the_serial_slot(stream_data):
+    """Calls without HS_KIND_FLAG_CHAINED wait for their predecessor before loading, so
+    they use the serial slot: the call counter does not move, no slot is released, and
+    interleaving them with chained (rotating) calls keeps every count exact."""
+    torch, buf, host = stream_data
+    L = N.lib()
+    ws = torch.zeros(int(L.hs_workspace_bytes(64)), dtype=torch.uint8, device="cuda")
+    sizes = [4096, 1 << 16, 1 << 20, 4 << 20, 16 << 20]
+    outs = torch.zeros((2 * len(sizes), 256), dtype=torch.int64, device="cuda")
+    for k, size in enumerate(sizes):
+        _issue(L, torch, buf, [4096 * k], [4096 * k + size], N.HS_KIND_NAIVE, ws, outs[k:k + 1])
+    torch.cuda.synchronize()
+    head = ws[:WS_HEAD_BYTES].cpu().numpy()
+    assert int(head[:8].view(np.uint64)[0]) == 0
+    assert not head[WS_DRAINED].view(np.uint32).any()
+    for k, size in enumerate(sizes):  # now alternate waiting and chained calls
+        kind = N.HS_KIND_NAIVE | (N.HS_KIND_FLAG_CHAINED if k % 2 else 0)
+        _issue(L, torch, buf, [8192 * k], [8192 * k + size], kind, ws, outs[len(sizes) + k:len(sizes) + k + 1])
+    torch.cuda.synchronize()
+    got = outs.cpu().numpy().view(np.uint64)
+    for k, size in enumerate(sizes):
+        assert np.array_equal(got[k], _counts(host, 4096 * k, 4096 * k + size))
+        assert np.array_equal(got[len(sizes) + k], _counts(host, 8192 * k, 8192 * k + size))
+    head = ws[:WS_HEAD_BYTES].cpu().numpy()
+    assert int(head[:8].view(np.uint64)[0]) == 4096 * (len(sizes) // 2)  # the chained calls only
     assert ws_clean(ws)
